@@ -1,0 +1,162 @@
+/*
+ * curvigpu.h — C ABI of libcurvigpu.so, the B200 (sm_100a) engine for the
+ * split exponential Euler hot path of arXiv 2604.11558 (reference package
+ * `curvipat`, pure Python; paths below are relative to
+ * /root/reference/pkg/src/curvipat).
+ *
+ * The reference has no FFI: its seams are Python functions.  Each entry point
+ * here replaces one of them; the Python drop-in (paper_2604_11558_b200/
+ * integrators.py) binds these with ctypes under the reference's names.
+ *
+ *   cg_plan_create      replaces prepare()            integrators.py:130-173
+ *                       (operands are computed on the host, as north_star
+ *                        allows, and uploaded once)
+ *   cg_apply_diffusion  replaces apply_diffusion()    integrators.py:176-199
+ *   cg_kinetics         replaces CoupledSystem.kinetics closures
+ *                                                     models.py:386-391,
+ *                                                     :284-319, :528-532
+ *   cg_step             replaces step_split()         integrators.py:247-249
+ *                       (and the STEPPERS dispatch    integrators.py:239-244)
+ *   cg_run              replaces the loop body of run_simulation()
+ *                                                     integrators.py:413-427
+ *                       (kinetics from the common state, step every
+ *                        component, divergence guard DIVERGENCE_LIMIT :33)
+ *   cg_rng_*            replaces Xoshiro256pp / Uniform / Normal
+ *                                                     models.py:55-130
+ *
+ * Conventions
+ *   - All field pointers are DEVICE pointers to fp64 arrays laid out
+ *     C-contiguous as [batch][ncomp][n1][n2](n3), reference axis order.
+ *   - `stream` is a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
+ *     all work is stream-ordered, nothing synchronises the host except
+ *     cg_plan_create/destroy.
+ *   - Return codes: 0 ok, CG_EINVAL bad argument, CG_ECUDA CUDA failure,
+ *     CG_EUNSUPPORTED unsupported configuration.  cg_last_error() gives the
+ *     thread-local message of the last failure.
+ *   - A plan is not thread-safe; use one plan per host thread.
+ */
+#ifndef CURVIGPU_H
+#define CURVIGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CG_OK 0
+#define CG_EINVAL (-1)
+#define CG_ECUDA (-2)
+#define CG_EUNSUPPORTED (-3)
+
+/* Geometry tags: Geometry enum, integrators.py:46-50 */
+#define CG_DISK 0
+#define CG_SPHERE 1
+#define CG_BALL 2
+#define CG_CYLINDER 3
+
+/* Pointwise reaction kinds (two species, evaluated on physical = lifted + lift
+ * values).  Parameter order per run in kin_params[b * nparams + i]:
+ *   CG_KIN_EXTERNAL     0  no reaction in cg_run; cg_step takes G explicitly
+ *   CG_KIN_SCHNAKENBERG 1  gamma, a, b:  gamma(a-u+u^2v), gamma(b-u^2v)
+ *                          (models.py:293-296 scaled as in :528-532)
+ *   CG_KIN_BRUSSELATOR  2  A, B:  A-(B+1)u+u^2v, Bu-u^2v
+ *   CG_KIN_GRAY_SCOTT   3  F, k:  -uv^2+F(1-u), uv^2-(F+k)v
+ *   CG_KIN_BVAM_ETA     4  eta, a, b, h, C:
+ *                          eta(u+av-Cuv-uv^2), eta(bv+hu+Cuv+uv^2)
+ *   CG_KIN_BVAM         5  alpha1, alpha2, alpha3, beta1, beta2 (models.py:284-290)
+ *   CG_KIN_DIB          6  zeta1..zeta5, eta1, eta2, eta3, eta5 (models.py:299-319,
+ *                          times zeta1 as in :555-557)
+ */
+#define CG_KIN_EXTERNAL 0
+#define CG_KIN_SCHNAKENBERG 1
+#define CG_KIN_BRUSSELATOR 2
+#define CG_KIN_GRAY_SCOTT 3
+#define CG_KIN_BVAM_ETA 4
+#define CG_KIN_BVAM 5
+#define CG_KIN_DIB 6
+
+typedef struct cg_plan cg_plan;
+
+/* Host-side description of a batched split-EE problem: `batch` independent
+ * runs of the same `ncomp`-component system.  All pointers are HOST pointers;
+ * cg_plan_create copies them into plan-owned device memory.  Operators may
+ * differ per component (leading [ncomp] index), as ComponentOps allows
+ * (integrators.py:53-84).  Arrays a geometry does not use may be NULL.
+ * n_rho / n_theta / n_phi / n_z below mean the extent of that axis. */
+typedef struct {
+  int geometry;           /* CG_DISK .. CG_CYLINDER */
+  int n[3];               /* reference axis order; n[2] = 1 for 2-D */
+  int batch;              /* runs */
+  int ncomp;              /* components (2 for every kinetics kind) */
+  double tau;
+  const double* coeff;    /* [ncomp] diffusion coefficients */
+  /* stencils for the diffusion action (bands a, b, c of TridiagonalOperator,
+   * operators.py:37-69; b and c have n-1 meaningful entries, stored in a
+   * row of length n): [ncomp][3][n_axis] */
+  const double* rho_bands;
+  const double* phi_bands;
+  const double* z_bands;
+  const double* theta_stencil; /* [ncomp][2] = (diag, off) of PeriodicTridiagonal */
+  const double* d_rho;    /* [ncomp][n_rho] rho weights (rho^-2 or rho^-(2+lambda)) */
+  const double* d_phi;    /* [ncomp][n_phi] sin^-2(phi) */
+  /* dense transforms as prepare() builds them */
+  const double* Q_theta;  /* [ncomp][n_theta][n_theta] */
+  const double* phi1_rho; /* [ncomp][n_rho][n_rho] */
+  const double* phi1_phi; /* [ncomp][n_phi][n_phi]  (sphere) */
+  const double* phi1_z;   /* [ncomp][n_z][n_z]      (cylinder) */
+  const double* V_phi;    /* [ncomp][n_phi][n_phi]  (ball) */
+  const double* Vinv_phi; /* [ncomp][n_phi][n_phi]  (ball) */
+  /* phi1 tensors (PhiTensor.field, phifun.py:52-65), per component:
+   *   disk [n_rho][n_theta]; sphere [n_theta][n_phi];
+   *   ball Phi [n_rho][n_theta][n_phi] and Phi_outer [n_rho][n_phi]
+   *        (constant along theta, stored 2-D);
+   *   cylinder [n_rho][n_theta] (constant along z, stored 2-D) */
+  const double* Phi;
+  const double* Phi_outer;
+  int kinetics;           /* CG_KIN_* */
+  int nparams;
+  const double* kin_params; /* [batch][nparams] */
+  const double* lift;     /* [ncomp] constant lift restoring physical values */
+} cg_desc;
+
+int cg_plan_create(const cg_desc* desc, cg_plan** out);
+void cg_plan_destroy(cg_plan* plan);
+
+/* Elements of one [batch][ncomp][...] state array. */
+long long cg_plan_state_elems(const cg_plan* plan);
+
+/* out = coeff * M W for every field (apply_diffusion, integrators.py:176-199). */
+int cg_apply_diffusion(cg_plan* plan, const double* W, double* out, void* stream);
+
+/* G = g(W + lift) for every run (the kinetics closure). */
+int cg_kinetics(cg_plan* plan, const double* W, double* G, void* stream);
+
+/* W_out = step_split(W, G) for every field; W_out must not alias W. */
+int cg_step(cg_plan* plan, const double* W, const double* G, double* W_out, void* stream);
+
+/* Advance `state` (in place) by nsteps split-EE steps with the plan's
+ * kinetics, steps numbered step0+1 .. step0+nsteps.  first_bad ([batch*ncomp]
+ * device ints) receives, per field, the smallest step whose result was
+ * non-finite or exceeded 1e12 in magnitude (atomicMin; callers initialise it
+ * to INT32_MAX).  The step sequence is replayed from CUDA graphs. */
+int cg_run(cg_plan* plan, double* state, long long step0, long long nsteps,
+           int* first_bad, void* stream);
+
+/* Last error message of the calling thread. */
+const char* cg_last_error(void);
+int cg_version(void);
+
+/* Host RNG: xoshiro256++ seeded through splitmix64 (models.py:43-104).
+ * state is 4 uint64 words owned by the caller. */
+void cg_rng_seed(uint64_t seed, uint64_t state[4]);
+void cg_rng_next(uint64_t state[4], long long n, uint64_t* out);
+/* lo + (hi - lo) * U[0,1) (models.py:107-119) */
+void cg_rng_uniform(uint64_t state[4], long long n, double lo, double hi, double* out);
+/* sigma * Box-Muller normal (models.py:93-104, :121-130) */
+void cg_rng_normal(uint64_t state[4], long long n, double sigma, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CURVIGPU_H */

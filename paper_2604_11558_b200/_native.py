@@ -1,0 +1,137 @@
+"""ctypes binding of libcurvigpu.so (C ABI in include/curvigpu.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (or
+``python -m paper_2604_11558_b200.build``).  There is no fallback: if the
+shared object is missing or a call fails, an exception is raised.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libcurvigpu.so"
+
+CG_OK = 0
+CG_EINVAL = -1
+CG_ECUDA = -2
+CG_EUNSUPPORTED = -3
+
+GEOMETRY_CODES = {"disk": 0, "sphere": 1, "ball": 2, "cylinder": 3}
+
+
+class EngineError(RuntimeError):
+    """A libcurvigpu call failed (message from cg_last_error)."""
+
+
+class cg_desc(ctypes.Structure):
+    _dp = ctypes.POINTER(ctypes.c_double)
+    _fields_ = [
+        ("geometry", ctypes.c_int),
+        ("n", ctypes.c_int * 3),
+        ("batch", ctypes.c_int),
+        ("ncomp", ctypes.c_int),
+        ("tau", ctypes.c_double),
+        ("coeff", _dp),
+        ("rho_bands", _dp),
+        ("phi_bands", _dp),
+        ("z_bands", _dp),
+        ("theta_stencil", _dp),
+        ("d_rho", _dp),
+        ("d_phi", _dp),
+        ("Q_theta", _dp),
+        ("phi1_rho", _dp),
+        ("phi1_phi", _dp),
+        ("phi1_z", _dp),
+        ("V_phi", _dp),
+        ("Vinv_phi", _dp),
+        ("Phi", _dp),
+        ("Phi_outer", _dp),
+        ("kinetics", ctypes.c_int),
+        ("nparams", ctypes.c_int),
+        ("kin_params", _dp),
+        ("lift", _dp),
+    ]
+
+
+_lib = None
+
+EXPORTS = (
+    "cg_plan_create",
+    "cg_plan_destroy",
+    "cg_plan_state_elems",
+    "cg_apply_diffusion",
+    "cg_kinetics",
+    "cg_step",
+    "cg_run",
+    "cg_last_error",
+    "cg_version",
+    "cg_rng_seed",
+    "cg_rng_next",
+    "cg_rng_uniform",
+    "cg_rng_normal",
+)
+
+
+def lib():
+    """Load (once) and return the shared library; raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = os.environ.get("CURVIGPU_LIB", str(LIB_PATH))
+    if not os.path.exists(path):
+        raise EngineError(
+            f"{path} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)"
+        )
+    L = ctypes.CDLL(path)
+    vp = ctypes.c_void_p
+    dp = ctypes.POINTER(ctypes.c_double)
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    L.cg_plan_create.argtypes = [ctypes.POINTER(cg_desc), ctypes.POINTER(vp)]
+    L.cg_plan_create.restype = ctypes.c_int
+    L.cg_plan_destroy.argtypes = [vp]
+    L.cg_plan_destroy.restype = None
+    L.cg_plan_state_elems.argtypes = [vp]
+    L.cg_plan_state_elems.restype = ctypes.c_longlong
+    L.cg_apply_diffusion.argtypes = [vp, vp, vp, vp]
+    L.cg_apply_diffusion.restype = ctypes.c_int
+    L.cg_kinetics.argtypes = [vp, vp, vp, vp]
+    L.cg_kinetics.restype = ctypes.c_int
+    L.cg_step.argtypes = [vp, vp, vp, vp, vp]
+    L.cg_step.restype = ctypes.c_int
+    L.cg_run.argtypes = [vp, vp, ctypes.c_longlong, ctypes.c_longlong, vp, vp]
+    L.cg_run.restype = ctypes.c_int
+    L.cg_last_error.argtypes = []
+    L.cg_last_error.restype = ctypes.c_char_p
+    L.cg_version.argtypes = []
+    L.cg_version.restype = ctypes.c_int
+    L.cg_rng_seed.argtypes = [ctypes.c_uint64, u64p]
+    L.cg_rng_seed.restype = None
+    L.cg_rng_next.argtypes = [u64p, ctypes.c_longlong, u64p]
+    L.cg_rng_next.restype = None
+    L.cg_rng_uniform.argtypes = [u64p, ctypes.c_longlong, ctypes.c_double, ctypes.c_double, dp]
+    L.cg_rng_uniform.restype = None
+    L.cg_rng_normal.argtypes = [u64p, ctypes.c_longlong, ctypes.c_double, dp]
+    L.cg_rng_normal.restype = None
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str) -> None:
+    if rc != CG_OK:
+        msg = lib().cg_last_error().decode(errors="replace")
+        if rc == CG_EINVAL:
+            raise ValueError(f"{what}: {msg}")
+        if rc == CG_EUNSUPPORTED:
+            raise NotImplementedError(f"{what}: {msg}")
+        raise EngineError(f"{what} failed ({rc}): {msg}")
+
+
+def dptr(arr):
+    """ctypes double* for a C-contiguous float64 numpy array (or None)."""
+    if arr is None:
+        return None
+    return arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))

@@ -1,0 +1,250 @@
+// Batched fp64 mu-mode product kernels for sm_100a.
+//
+// Every mu-mode product of the split exponential Euler step
+// (integrators.py:202-236, tensor.py:31-49) is one of two GEMM shapes over
+// the C-contiguous [field][n1][n2](n3) state, so no tensor is ever permuted:
+//
+//   TN  ("right" product, last mode):  Y[f](rows x N) = X[f](rows x K) . B^T
+//       A = state rows (K contiguous), B = operator stored [N][K].
+//   NN  ("left" product, first/middle mode): Y[f,s](M x N) = L(M x K) . X[f,s](K x N)
+//       A = operator stored transposed [K][M], B = state slab [K][N].
+//
+// fp64 has no tcgen05 kind (ptxas rejects .kind::f64), so the tensor-core
+// path is warp-level DMMA (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4), measured
+// at 37.05 TFLOP/s on B200 (profiles/r01_fp64_peak.txt).  Operand tiles are
+// staged by TMA (cp.async.bulk.tensor, 128B swizzle, zero fill out of bounds
+// so n = 100 needs no host padding) into a STAGES-deep mbarrier ring fed by
+// one producer warp; consumer warps read register fragments with
+// conflict-free 8-byte shared loads (the fragment-to-row map below is chosen
+// against the swizzle so every half-warp touches 16 distinct bank pairs).
+//
+// Epilogues are fused: plain store, Hadamard with a phi1 tensor (the "T *=
+// Phi" of the steppers), or the final "W + tau * T" with the divergence
+// guard of run_simulation (integrators.py:422-427).
+#pragma once
+
+#include "common.cuh"
+
+namespace cg {
+
+enum { VAR_TN = 0, VAR_NN = 1 };
+enum { EPI_STORE = 0, EPI_PHI = 1, EPI_AXPY = 2 };
+
+struct GemmParams {
+  int M, N, K;
+  int nslab;   // batch item t -> field f = t / nslab, slab s = t % nslab
+  int ncomp;   // component c = f % ncomp
+  int nbatch;  // nfield * nslab
+  int tiles_m, tiles_n;
+  double* out;
+  long long out_f, out_s;  // element strides of field / slab in out (and w)
+  int ldc;
+  const double* w;  // EPI_AXPY: previous state, same indexing as out
+  const double* phi;  // EPI_PHI: phi + c*phi_c + s*phi_s + (m/phi_rdiv)*phi_m + n*phi_n
+  long long phi_c, phi_s;
+  int phi_m, phi_n, phi_rdiv;
+  double tau, limit;
+  int* first_bad;   // [nfield] smallest diverged step (atomicMin)
+  const int* step;  // current step number (device)
+};
+
+template <int BM, int BN>
+struct StageBytes {
+  static constexpr int A = BM * 128;  // BM x 16 doubles (TN) == BM/16 boxes of 16x16 (NN)
+  static constexpr int B = BN * 128;
+  static constexpr int total = A + B;
+};
+
+template <int BM, int BN, int STAGES>
+constexpr int gemm_smem_bytes() {
+  return STAGES * StageBytes<BM, BN>::total + 2 * STAGES * 8 + 1024;
+}
+
+// Row permutation within an 8-row group used by the TN fragments: rows of a
+// half-warp land on distinct 128B-swizzle phases.
+__device__ __forceinline__ int perm8(int g) { return ((g & 3) << 1) | (g >> 2); }
+
+template <int VAR, int BM, int BN, int WM, int WN, int STAGES, int EPI, int MINB>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
+    gemm_f64_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                    const GemmParams p) {
+  constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+  constexpr int NCW = WARPS_M * WARPS_N;  // consumer warps
+  constexpr int MT = WM / 8, NT = WN / 8;
+  constexpr int SA = StageBytes<BM, BN>::A, SB = StageBytes<BM, BN>::B;
+  constexpr int STAGE = SA + SB;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint64_t* empty = full + STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // tile decode: bid -> (batch item, m tile, n tile), n fastest
+  int bid = blockIdx.x;
+  const int tn = bid % p.tiles_n;
+  bid /= p.tiles_n;
+  const int tm = bid % p.tiles_m;
+  const int t = bid / p.tiles_m;
+  const int f = t / p.nslab, s = t - f * p.nslab;
+  const int c = f % p.ncomp;
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int KT = (p.K + 15) >> 4;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NCW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == NCW) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      tma_prefetch_desc(&mapA);
+      tma_prefetch_desc(&mapB);
+      for (int kt = 0; kt < KT; ++kt) {
+        const int st = kt % STAGES;
+        if (kt >= STAGES) mbar_wait(&empty[st], ((kt / STAGES) - 1) & 1);
+        uint8_t* sa = smem + st * STAGE;
+        uint8_t* sb = sa + SA;
+        mbar_arrive_expect_tx(&full[st], STAGE);
+        if (VAR == VAR_TN) {
+          tma_load_3d(sa, &mapA, &full[st], kt * 16, m0, f);
+          tma_load_3d(sb, &mapB, &full[st], kt * 16, n0, c);
+        } else {
+#pragma unroll
+          for (int q = 0; q < BM / 16; ++q) tma_load_3d(sa + q * 2048, &mapA, &full[st], m0 + 16 * q, kt * 16, c);
+#pragma unroll
+          for (int q = 0; q < BN / 16; ++q) tma_load_4d(sb + q * 2048, &mapB, &full[st], n0 + 16 * q, kt * 16, s, f);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- DMMA consumers ----------------
+  const int wy = warp / WARPS_N, wx = warp % WARPS_N;
+  const int wm0 = wy * WM, wn0 = wx * WN;
+  const int g = lane >> 2, tq = lane & 3;
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    const int st = kt % STAGES;
+    mbar_wait(&full[st], (kt / STAGES) & 1);
+    const double* sa = reinterpret_cast<const double*>(smem + st * STAGE);
+    const double* sb = reinterpret_cast<const double*>(smem + st * STAGE + SA);
+    if (VAR == VAR_TN) {
+      const int pg = perm8(g);
+#pragma unroll
+      for (int kk = 0; kk < 16; kk += 4) {
+        const int col = kk + tq;
+        const int off = ((((col >> 1) ^ pg)) << 1) | (col & 1);
+        double a[MT], b[NT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) a[i] = sa[(wm0 + i * 8 + pg) * 16 + off];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) b[j] = sb[(wn0 + j * 8 + pg) * 16 + off];
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
+    } else {
+#pragma unroll
+      for (int k8 = 0; k8 < 16; k8 += 8) {
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub) {
+          const int k = k8 + 2 * tq + sub;
+          const int kx = k & 7;
+          double a[MT], b[NT];
+#pragma unroll
+          for (int i = 0; i < MT; ++i) {
+            const int m = wm0 + i * 8 + g;
+            const int mm = m & 15;
+            a[i] = sa[(m >> 4) * 256 + k * 16 + ((((mm >> 1) ^ kx)) << 1) + (mm & 1)];
+          }
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const int n = wn0 + j * 8 + g;
+            const int nn = n & 15;
+            b[j] = sb[(n >> 4) * 256 + k * 16 + ((((nn >> 1) ^ kx)) << 1) + (nn & 1)];
+          }
+#pragma unroll
+          for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+
+  // ---------------- fused epilogue ----------------
+  int col_in8;
+  if (VAR == VAR_TN) {
+    // thread holds cols perm8(2t), perm8(2t+1) = {0,2},{4,6},{1,3},{5,7};
+    // swap with lane^2 so each thread owns an adjacent pair.
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const bool hi = (tq & 2) != 0;
+        const double send = hi ? acc[i][j][0] : acc[i][j][1];
+        const double recv = __shfl_xor_sync(0xffffffffu, send, 2);
+        if (hi)
+          acc[i][j][0] = recv;
+        else
+          acc[i][j][1] = recv;
+      }
+    col_in8 = ((tq & 1) << 2) | (tq & 2);
+  } else {
+    col_in8 = 2 * tq;
+  }
+  const int row_in8 = (VAR == VAR_TN) ? perm8(g) : g;
+
+  const long long base = (long long)f * p.out_f + (long long)s * p.out_s;
+  bool bad = false;
+  int step_now = 0;
+  if (EPI == EPI_AXPY) step_now = *p.step;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int m = m0 + wm0 + i * 8 + row_in8;
+    if (m >= p.M) continue;
+    const double* phirow = nullptr;
+    if (EPI == EPI_PHI)
+      phirow = p.phi + c * p.phi_c + s * p.phi_s + (long long)(m / p.phi_rdiv) * p.phi_m;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int n = n0 + wn0 + j * 8 + col_in8;
+      if (n >= p.N) continue;
+      const long long idx = base + (long long)m * p.ldc + n;
+      double v0 = acc[i][j][0], v1 = acc[i][j][1];
+      if (EPI == EPI_PHI) {
+        v0 *= __ldg(phirow + (long long)n * p.phi_n);
+        v1 *= __ldg(phirow + (long long)(n + 1) * p.phi_n);
+      } else if (EPI == EPI_AXPY) {
+        const double2 w2 = __ldg(reinterpret_cast<const double2*>(p.w + idx));
+        // W + tau*T rounded as the reference rounds it (no FMA contraction)
+        v0 = __dadd_rn(w2.x, __dmul_rn(p.tau, v0));
+        v1 = __dadd_rn(w2.y, __dmul_rn(p.tau, v1));
+        bad |= !(fabs(v0) <= p.limit) || !(fabs(v1) <= p.limit);
+      }
+      *reinterpret_cast<double2*>(p.out + idx) = make_double2(v0, v1);
+    }
+  }
+  if (EPI == EPI_AXPY) {
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(p.first_bad + f, step_now);
+  }
+}
+
+}  // namespace cg

@@ -1,0 +1,731 @@
+// libcurvigpu: plan construction, per-geometry step schedules, CUDA-graph
+// time loop and the C ABI declared in include/curvigpu.h.
+//
+// One step of the reference (run_simulation loop body, integrators.py:413-427)
+// becomes:
+//   fbuild            F = coeff*M W + g(W+lift)      (HBM-bound stencil pass)
+//   2..5 GEMM stages  the geometry's mu-mode chain    (DMMA, TMA-fed)
+//                     (integrators.py:202-236), the last one fused with
+//                     W + tau*T and the divergence guard
+// and the whole sequence is captured once into a CUDA graph and replayed.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "curvigpu.h"
+#include "gemm.cuh"
+#include "stencil.cuh"
+
+using namespace cg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                         \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(CG_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_) + " @" + \
+                                std::to_string(__LINE__));                                  \
+  } while (0)
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// fp64 tensor map, 128B swizzle, zero fill; dims innermost first, strides in bytes.
+int make_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+             const uint32_t* box) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(CG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t gd[5], gs[4];
+  cuuint32_t bx[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+    es[i] = 1;
+  }
+  for (int i = 0; i < rank - 1; ++i) gs[i] = strides_bytes[i];
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), gd, gs, bx, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CG_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return CG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// GEMM tile configurations and dispatch
+// ---------------------------------------------------------------------------
+
+struct TileCfg {
+  int BM, BN;
+};
+constexpr int kNumCfg = 3;
+constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}};
+
+// BM, BN, warp tile, stages; 32x32 warp tiles keep the accumulators +
+// fragments under ~160 registers without spills.
+#define CFG0 128, 64, 32, 32, 4
+#define CFG1 64, 128, 32, 32, 4
+#define CFG2 64, 64, 32, 32, 4
+
+// configure_only: set the dynamic shared memory opt-in (done at plan
+// creation, never inside a stream capture).
+template <int VAR, int BM, int BN, int WM, int WN, int ST, int EPI>
+int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams& p, cudaStream_t stream,
+                  bool configure_only) {
+  constexpr int MINB = ((BM / WM) * (BN / WN) <= 4) ? 2 : 1;
+  auto kern = gemm_f64_kernel<VAR, BM, BN, WM, WN, ST, EPI, MINB>;
+  constexpr int smem = gemm_smem_bytes<BM, BN, ST>();
+  if (configure_only) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    return CG_OK;
+  }
+  const long long blocks = (long long)p.nbatch * p.tiles_m * p.tiles_n;
+  if (blocks <= 0) return CG_OK;
+  if (blocks > INT_MAX) return fail(CG_EUNSUPPORTED, "grid too large");
+  constexpr int threads = (BM / WM) * (BN / WN) * 32 + 32;
+  kern<<<(unsigned)blocks, threads, smem, stream>>>(ma, mb, p);
+  CUDA_TRY(cudaGetLastError());
+  return CG_OK;
+}
+
+template <int VAR, int EPI>
+int launch_gemm_cfg(int cfg, const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams& p,
+                    cudaStream_t stream, bool conf) {
+  switch (cfg) {
+    case 0: return launch_gemm_t<VAR, CFG0, EPI>(ma, mb, p, stream, conf);
+    case 1: return launch_gemm_t<VAR, CFG1, EPI>(ma, mb, p, stream, conf);
+    default: return launch_gemm_t<VAR, CFG2, EPI>(ma, mb, p, stream, conf);
+  }
+}
+
+int launch_gemm(int var, int epi, int cfg, const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams& p,
+                cudaStream_t s, bool conf = false) {
+  if (var == VAR_TN) {
+    if (epi == EPI_STORE) return launch_gemm_cfg<VAR_TN, EPI_STORE>(cfg, ma, mb, p, s, conf);
+    if (epi == EPI_PHI) return launch_gemm_cfg<VAR_TN, EPI_PHI>(cfg, ma, mb, p, s, conf);
+    return launch_gemm_cfg<VAR_TN, EPI_AXPY>(cfg, ma, mb, p, s, conf);
+  }
+  if (epi == EPI_STORE) return launch_gemm_cfg<VAR_NN, EPI_STORE>(cfg, ma, mb, p, s, conf);
+  if (epi == EPI_PHI) return launch_gemm_cfg<VAR_NN, EPI_PHI>(cfg, ma, mb, p, s, conf);
+  return launch_gemm_cfg<VAR_NN, EPI_AXPY>(cfg, ma, mb, p, s, conf);
+}
+
+__global__ void set_step_kernel(int* step, int value) { *step = value; }
+
+template <int GEOM, int KIN>
+int launch_fbuild_t(const StencilParams& p, cudaStream_t s) {
+  const long long total = p.npts * p.batch;
+  long long blocks = (total + 255) / 256;
+  const long long cap = 148LL * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  fbuild_kernel<GEOM, KIN><<<(unsigned)blocks, 256, 0, s>>>(p);
+  CUDA_TRY(cudaGetLastError());
+  return CG_OK;
+}
+
+template <int GEOM>
+int launch_fbuild_g(int kin, const StencilParams& p, cudaStream_t s) {
+  switch (kin) {
+    case KIN_SCHNAKENBERG: return launch_fbuild_t<GEOM, KIN_SCHNAKENBERG>(p, s);
+    case KIN_BRUSSELATOR: return launch_fbuild_t<GEOM, KIN_BRUSSELATOR>(p, s);
+    case KIN_GRAY_SCOTT: return launch_fbuild_t<GEOM, KIN_GRAY_SCOTT>(p, s);
+    case KIN_BVAM_ETA: return launch_fbuild_t<GEOM, KIN_BVAM_ETA>(p, s);
+    case KIN_BVAM: return launch_fbuild_t<GEOM, KIN_BVAM>(p, s);
+    case KIN_DIB: return launch_fbuild_t<GEOM, KIN_DIB>(p, s);
+    default: return launch_fbuild_t<GEOM, KIN_EXTERNAL>(p, s);
+  }
+}
+
+int launch_fbuild(int geom, int kin, const StencilParams& p, cudaStream_t s) {
+  switch (geom) {
+    case CG_DISK: return launch_fbuild_g<0>(kin, p, s);
+    case CG_SPHERE: return launch_fbuild_g<1>(kin, p, s);
+    case CG_BALL: return launch_fbuild_g<2>(kin, p, s);
+    default: return launch_fbuild_g<3>(kin, p, s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+
+enum { BUF_X = 0, BUF_Y = 1, BUF_OUT = 2 };
+
+struct Stage {
+  int var, epi, cfg;
+  int M, N, K, nslab;
+  int src, dst;  // BUF_X / BUF_Y / BUF_OUT
+  const double* phi;
+  long long phi_c, phi_s;
+  int phi_m, phi_n, phi_rdiv;
+  CUtensorMap opmap;  // operator operand (B for TN, A for NN)
+};
+
+struct GraphEntry {
+  double* state;
+  int* first_bad;
+  cudaGraphExec_t chunk;
+};
+
+constexpr int kChunk = 16;  // steps per captured graph (even)
+
+}  // namespace
+
+struct cg_plan {
+  int geom, n1, n2, n3, B, C, kin, P;
+  double tau;
+  long long npts, elems;
+  std::vector<void*> allocs;
+  double *coeff = nullptr, *lift = nullptr, *kin_params = nullptr;
+  double *rho_b = nullptr, *phi_b = nullptr, *z_b = nullptr, *th = nullptr, *d_rho = nullptr, *d_phi = nullptr;
+  double *X = nullptr, *Y = nullptr, *S2 = nullptr;
+  int* step_dev = nullptr;
+  int* scratch_bad = nullptr;
+  std::vector<Stage> stages;
+  std::vector<GraphEntry> graphs;
+  cudaStream_t cap_stream = nullptr;
+};
+
+namespace {
+
+int dev_alloc(cg_plan* p, size_t bytes, void** out) {
+  CUDA_TRY(cudaMalloc(out, bytes == 0 ? 16 : bytes));
+  p->allocs.push_back(*out);
+  return CG_OK;
+}
+
+int upload(cg_plan* p, const double* host, size_t count, double** out) {
+  if (!host) {
+    *out = nullptr;
+    return CG_OK;
+  }
+  int rc = dev_alloc(p, count * sizeof(double), reinterpret_cast<void**>(out));
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpy(*out, host, count * sizeof(double), cudaMemcpyHostToDevice));
+  return CG_OK;
+}
+
+// Operator for a TN stage, stored [C][N][Kp] with Kp = even(K): op[c][n][k] = src(c, n, k).
+// Operator for a NN stage, stored [C][K][Mp]: op[c][k][m] = L_c[m][k].
+// `get(c, r, q)` returns L_c[r][q] (row r, col q) of the n x n left matrix.
+template <typename Get>
+int upload_operator(cg_plan* p, int var, int n, Get get, double** out, CUtensorMap* map, int box_rows) {
+  const int np = (n + 1) & ~1;
+  std::vector<double> h((size_t)p->C * n * np, 0.0);
+  for (int c = 0; c < p->C; ++c)
+    for (int r = 0; r < n; ++r)
+      for (int q = 0; q < n; ++q) {
+        // TN: B[n_out = r][k = q] = L[r][q];  NN: A^T[k = q][m = r] = L[r][q]
+        if (var == VAR_TN)
+          h[((size_t)c * n + r) * np + q] = get(c, r, q);
+        else
+          h[((size_t)c * n + q) * np + r] = get(c, r, q);
+      }
+  int rc = upload(p, h.data(), h.size(), out);
+  if (rc) return rc;
+  const uint64_t dims[3] = {(uint64_t)n, (uint64_t)n, (uint64_t)p->C};
+  const uint64_t strides[2] = {(uint64_t)np * 8, (uint64_t)n * np * 8};
+  const uint32_t box[3] = {16, (uint32_t)box_rows, 1};
+  return make_map(map, *out, 3, dims, strides, box);
+}
+
+int pick_cfg(int var, long long nbatch, int M, int N) {
+  // largest tile that still gives >= 2 waves of 148 SMs (or the smallest tile)
+  for (int c = 0; c < kNumCfg; ++c) {
+    const long long ctas = nbatch * ((M + kCfgs[c].BM - 1) / kCfgs[c].BM) * ((N + kCfgs[c].BN - 1) / kCfgs[c].BN);
+    if (ctas >= 2 * 148) return c;
+  }
+  (void)var;
+  return kNumCfg - 1;
+}
+
+// Build one GEMM stage: operator L (n x n) via `get`, shapes, epilogue.
+template <typename Get>
+int add_stage(cg_plan* p, int var, int epi, int M, int N, int K, int nslab, int src, int dst, int n_op, Get get) {
+  Stage st{};
+  st.var = var;
+  st.epi = epi;
+  st.M = M;
+  st.N = N;
+  st.K = K;
+  st.nslab = nslab;
+  st.src = src;
+  st.dst = dst;
+  st.phi_rdiv = 1;
+  const long long nbatch = (long long)p->B * p->C * nslab;
+  st.cfg = pick_cfg(var, nbatch, M, N);
+  double* op = nullptr;
+  const int box_rows = (var == VAR_TN) ? kCfgs[st.cfg].BN : 16;
+  int rc = upload_operator(p, var, n_op, get, &op, &st.opmap, box_rows);
+  if (rc) return rc;
+  p->stages.push_back(st);
+  return CG_OK;
+}
+
+double* buf_ptr(cg_plan* p, int id, double* out) { return id == BUF_X ? p->X : id == BUF_Y ? p->Y : out; }
+
+// Launch one full step: Win (+G) -> F -> stage chain -> Wout.
+int launch_step(cg_plan* p, const double* Win, double* Wout, const double* Gext, bool fused_kin, int* first_bad,
+                bool count_step, cudaStream_t s) {
+  StencilParams sp{};
+  sp.geometry = p->geom;
+  sp.n1 = p->n1;
+  sp.n2 = p->n2;
+  sp.n3 = p->n3;
+  sp.ncomp = p->C;
+  sp.batch = p->B;
+  sp.npts = p->npts;
+  sp.rho_b = p->rho_b;
+  sp.phi_b = p->phi_b;
+  sp.z_b = p->z_b;
+  sp.th = p->th;
+  sp.d_rho = p->d_rho;
+  sp.d_phi = p->d_phi;
+  sp.coeff = p->coeff;
+  sp.lift = p->lift;
+  sp.kin = p->kin_params;
+  sp.nparams = p->P;
+  sp.W = Win;
+  sp.G = Gext;
+  sp.F = p->X;
+  sp.with_diffusion = 1;
+  sp.with_reaction = 1;
+  sp.step = count_step ? p->step_dev : nullptr;
+  int rc = launch_fbuild(p->geom, fused_kin ? p->kin : KIN_EXTERNAL, sp, s);
+  if (rc) return rc;
+
+  for (const Stage& st : p->stages) {
+    const double* src = buf_ptr(p, st.src, Wout);
+    double* dst = buf_ptr(p, st.dst, Wout);
+    CUtensorMap smap;
+    const TileCfg tc = kCfgs[st.cfg];
+    const long long nfield = (long long)p->B * p->C;
+    if (st.var == VAR_TN) {
+      // state as (K, rows, field)
+      const uint64_t dims[3] = {(uint64_t)st.K, (uint64_t)st.M, (uint64_t)nfield};
+      const uint64_t strides[2] = {(uint64_t)st.K * 8, (uint64_t)p->npts * 8};
+      const uint32_t box[3] = {16, (uint32_t)tc.BM, 1};
+      rc = make_map(&smap, src, 3, dims, strides, box);
+    } else {
+      // state as (N, K, slab, field)
+      const uint64_t dims[4] = {(uint64_t)st.N, (uint64_t)st.K, (uint64_t)st.nslab, (uint64_t)nfield};
+      const uint64_t strides[3] = {(uint64_t)st.N * 8, (uint64_t)st.K * st.N * 8, (uint64_t)p->npts * 8};
+      const uint32_t box[4] = {16, 16, 1, 1};
+      rc = make_map(&smap, src, 4, dims, strides, box);
+    }
+    if (rc) return rc;
+    GemmParams gp{};
+    gp.M = st.M;
+    gp.N = st.N;
+    gp.K = st.K;
+    gp.nslab = st.nslab;
+    gp.ncomp = p->C;
+    gp.nbatch = (int)(nfield * st.nslab);
+    gp.tiles_m = (st.M + tc.BM - 1) / tc.BM;
+    gp.tiles_n = (st.N + tc.BN - 1) / tc.BN;
+    gp.out = dst;
+    gp.out_f = p->npts;
+    gp.out_s = (long long)st.K * st.N;  // slab stride (NN middle mode: n2*n3 ... K*N)
+    gp.ldc = st.N;
+    gp.w = Win;
+    gp.phi = st.phi;
+    gp.phi_c = st.phi_c;
+    gp.phi_s = st.phi_s;
+    gp.phi_m = st.phi_m;
+    gp.phi_n = st.phi_n;
+    gp.phi_rdiv = st.phi_rdiv;
+    gp.tau = p->tau;
+    gp.limit = 1e12;  // DIVERGENCE_LIMIT, integrators.py:33
+    gp.first_bad = first_bad;
+    gp.step = p->step_dev;
+    if (st.var == VAR_TN)
+      rc = launch_gemm(st.var, st.epi, st.cfg, smap, st.opmap, gp, s);
+    else
+      rc = launch_gemm(st.var, st.epi, st.cfg, st.opmap, smap, gp, s);
+    if (rc) return rc;
+  }
+  return CG_OK;
+}
+
+int build_stages(cg_plan* p, const cg_desc* d) {
+  const int n1 = p->n1, n2 = p->n2, n3 = p->n3, C = p->C;
+  const double* Q = d->Q_theta;
+  auto need = [&](const void* ptr, const char* name) -> int {
+    if (!ptr) return fail(CG_EINVAL, std::string("missing operand ") + name);
+    return CG_OK;
+  };
+  int rc = 0;
+  // phi tables
+  auto up_phi = [&](const double* h, size_t per, double** out) -> int { return upload(p, h, per * C, out); };
+  if (p->geom == CG_DISK) {
+    const int nt = n2;
+    if ((rc = need(Q, "Q_theta")) || (rc = need(d->phi1_rho, "phi1_rho")) || (rc = need(d->Phi, "Phi"))) return rc;
+    double* phi = nullptr;
+    if ((rc = up_phi(d->Phi, (size_t)n1 * n2, &phi))) return rc;
+    // T = F Q  (L = Q^T: L[r][q] = Q[q][r]), epilogue *= Phi_c(i, j)
+    if ((rc = add_stage(p, VAR_TN, EPI_PHI, n1, n2, n2, 1, BUF_X, BUF_Y, nt,
+                        [&](int c, int r, int q) { return Q[((size_t)c * nt + q) * nt + r]; })))
+      return rc;
+    Stage& s0 = p->stages.back();
+    s0.phi = phi;
+    s0.phi_c = (long long)n1 * n2;
+    s0.phi_m = n2;
+    s0.phi_n = 1;
+    // T = T Q^T  (L = Q)
+    if ((rc = add_stage(p, VAR_TN, EPI_STORE, n1, n2, n2, 1, BUF_Y, BUF_X, nt,
+                        [&](int c, int r, int q) { return Q[((size_t)c * nt + r) * nt + q]; })))
+      return rc;
+    // W + tau * phi1_rho T
+    const double* P1 = d->phi1_rho;
+    if ((rc = add_stage(p, VAR_NN, EPI_AXPY, n1, n2, n1, 1, BUF_X, BUF_OUT, n1,
+                        [&](int c, int r, int q) { return P1[((size_t)c * n1 + r) * n1 + q]; })))
+      return rc;
+  } else if (p->geom == CG_SPHERE) {
+    const int nt = n1, np_ = n2;
+    if ((rc = need(Q, "Q_theta")) || (rc = need(d->phi1_phi, "phi1_phi")) || (rc = need(d->Phi, "Phi"))) return rc;
+    double* phi = nullptr;
+    if ((rc = up_phi(d->Phi, (size_t)n1 * n2, &phi))) return rc;
+    // T = Q^T F
+    if ((rc = add_stage(p, VAR_NN, EPI_STORE, n1, n2, n1, 1, BUF_X, BUF_Y, nt,
+                        [&](int c, int r, int q) { return Q[((size_t)c * nt + q) * nt + r]; })))
+      return rc;
+    // T = T phi1_phi^T, epilogue *= Phi_c(i, j)
+    const double* P1 = d->phi1_phi;
+    if ((rc = add_stage(p, VAR_TN, EPI_PHI, n1, n2, n2, 1, BUF_Y, BUF_X, np_,
+                        [&](int c, int r, int q) { return P1[((size_t)c * np_ + r) * np_ + q]; })))
+      return rc;
+    Stage& s1 = p->stages.back();
+    s1.phi = phi;
+    s1.phi_c = (long long)n1 * n2;
+    s1.phi_m = n2;
+    s1.phi_n = 1;
+    // W + tau * Q T
+    if ((rc = add_stage(p, VAR_NN, EPI_AXPY, n1, n2, n1, 1, BUF_X, BUF_OUT, nt,
+                        [&](int c, int r, int q) { return Q[((size_t)c * nt + r) * nt + q]; })))
+      return rc;
+  } else if (p->geom == CG_BALL) {
+    if ((rc = need(Q, "Q_theta")) || (rc = need(d->phi1_rho, "phi1_rho")) || (rc = need(d->Phi, "Phi")) ||
+        (rc = need(d->Phi_outer, "Phi_outer")) || (rc = need(d->V_phi, "V_phi")) ||
+        (rc = need(d->Vinv_phi, "Vinv_phi")))
+      return rc;
+    double *phi = nullptr, *phio = nullptr;
+    if ((rc = up_phi(d->Phi, (size_t)n1 * n2 * n3, &phi))) return rc;
+    if ((rc = up_phi(d->Phi_outer, (size_t)n1 * n3, &phio))) return rc;
+    const double *V = d->V_phi, *Vi = d->Vinv_phi, *P1 = d->phi1_rho;
+    // T = F x3 V^-1, epilogue *= Phi_outer_c(i, k)
+    if ((rc = add_stage(p, VAR_TN, EPI_PHI, n1 * n2, n3, n3, 1, BUF_X, BUF_Y, n3,
+                        [&](int c, int r, int q) { return Vi[((size_t)c * n3 + r) * n3 + q]; })))
+      return rc;
+    Stage& s0 = p->stages.back();
+    s0.phi = phio;
+    s0.phi_c = (long long)n1 * n3;
+    s0.phi_rdiv = n2;
+    s0.phi_m = n3;
+    s0.phi_n = 1;
+    // T = T x3 V
+    if ((rc = add_stage(p, VAR_TN, EPI_STORE, n1 * n2, n3, n3, 1, BUF_Y, BUF_X, n3,
+                        [&](int c, int r, int q) { return V[((size_t)c * n3 + r) * n3 + q]; })))
+      return rc;
+    // T = T x2 Q^T, epilogue *= Phi_c(i, j, k)
+    if ((rc = add_stage(p, VAR_NN, EPI_PHI, n2, n3, n2, n1, BUF_X, BUF_Y, n2,
+                        [&](int c, int r, int q) { return Q[((size_t)c * n2 + q) * n2 + r]; })))
+      return rc;
+    Stage& s2 = p->stages.back();
+    s2.phi = phi;
+    s2.phi_c = (long long)n1 * n2 * n3;
+    s2.phi_s = (long long)n2 * n3;
+    s2.phi_m = n3;
+    s2.phi_n = 1;
+    // T = T x2 Q
+    if ((rc = add_stage(p, VAR_NN, EPI_STORE, n2, n3, n2, n1, BUF_Y, BUF_X, n2,
+                        [&](int c, int r, int q) { return Q[((size_t)c * n2 + r) * n2 + q]; })))
+      return rc;
+    // W + tau * (T x1 phi1_rho)
+    if ((rc = add_stage(p, VAR_NN, EPI_AXPY, n1, n2 * n3, n1, 1, BUF_X, BUF_OUT, n1,
+                        [&](int c, int r, int q) { return P1[((size_t)c * n1 + r) * n1 + q]; })))
+      return rc;
+  } else {  // cylinder
+    if ((rc = need(Q, "Q_theta")) || (rc = need(d->phi1_rho, "phi1_rho")) || (rc = need(d->Phi, "Phi")) ||
+        (rc = need(d->phi1_z, "phi1_z")))
+      return rc;
+    double* phi = nullptr;
+    if ((rc = up_phi(d->Phi, (size_t)n1 * n2, &phi))) return rc;
+    const double *Pz = d->phi1_z, *P1 = d->phi1_rho;
+    // T = F x3 phi1_z
+    if ((rc = add_stage(p, VAR_TN, EPI_STORE, n1 * n2, n3, n3, 1, BUF_X, BUF_Y, n3,
+                        [&](int c, int r, int q) { return Pz[((size_t)c * n3 + r) * n3 + q]; })))
+      return rc;
+    // T = T x2 Q^T, epilogue *= Phi_c(i, j) (constant along z)
+    if ((rc = add_stage(p, VAR_NN, EPI_PHI, n2, n3, n2, n1, BUF_Y, BUF_X, n2,
+                        [&](int c, int r, int q) { return Q[((size_t)c * n2 + q) * n2 + r]; })))
+      return rc;
+    Stage& s1 = p->stages.back();
+    s1.phi = phi;
+    s1.phi_c = (long long)n1 * n2;
+    s1.phi_s = n2;
+    s1.phi_m = 1;
+    s1.phi_n = 0;
+    // T = T x2 Q
+    if ((rc = add_stage(p, VAR_NN, EPI_STORE, n2, n3, n2, n1, BUF_X, BUF_Y, n2,
+                        [&](int c, int r, int q) { return Q[((size_t)c * n2 + r) * n2 + q]; })))
+      return rc;
+    // W + tau * (T x1 phi1_rho)
+    if ((rc = add_stage(p, VAR_NN, EPI_AXPY, n1, n2 * n3, n1, 1, BUF_Y, BUF_OUT, n1,
+                        [&](int c, int r, int q) { return P1[((size_t)c * n1 + r) * n1 + q]; })))
+      return rc;
+  }
+  return CG_OK;
+}
+
+int bands_upload(cg_plan* p, const double* h, int n, double** out) { return upload(p, h, (size_t)p->C * 3 * n, out); }
+
+}  // namespace
+
+extern "C" {
+
+const char* cg_last_error(void) { return g_err.c_str(); }
+int cg_version(void) { return 1; }
+
+long long cg_plan_state_elems(const cg_plan* plan) { return plan ? plan->elems : 0; }
+
+void cg_plan_destroy(cg_plan* p) {
+  if (!p) return;
+  for (auto& g : p->graphs)
+    if (g.chunk) cudaGraphExecDestroy(g.chunk);
+  for (void* a : p->allocs) cudaFree(a);
+  if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+  delete p;
+}
+
+int cg_plan_create(const cg_desc* d, cg_plan** out) {
+  if (!d || !out) return fail(CG_EINVAL, "null argument");
+  *out = nullptr;
+  if (d->geometry < CG_DISK || d->geometry > CG_CYLINDER) return fail(CG_EINVAL, "unknown geometry");
+  const bool is3d = d->geometry == CG_BALL || d->geometry == CG_CYLINDER;
+  if (d->n[0] < 2 || d->n[1] < 2 || (is3d && d->n[2] < 2)) return fail(CG_EINVAL, "grid extents must be >= 2");
+  if (d->batch < 1 || d->ncomp < 1) return fail(CG_EINVAL, "batch and ncomp must be >= 1");
+  if (d->kinetics != CG_KIN_EXTERNAL && d->ncomp != 2)
+    return fail(CG_EUNSUPPORTED, "built-in kinetics kinds are two-species");
+  if (d->kinetics < CG_KIN_EXTERNAL || d->kinetics > CG_KIN_DIB) return fail(CG_EUNSUPPORTED, "unknown kinetics");
+  const int nlast = is3d ? d->n[2] : d->n[1];
+  if (nlast % 2 != 0)
+    return fail(CG_EUNSUPPORTED, "the contiguous (last) axis must have even extent (TMA 16-byte row strides)");
+  if (!(d->tau >= 0.0)) return fail(CG_EINVAL, "tau must be nonnegative");
+  if (!d->coeff || !d->lift) return fail(CG_EINVAL, "coeff and lift are required");
+
+  cg_plan* p = new cg_plan();
+  p->geom = d->geometry;
+  p->n1 = d->n[0];
+  p->n2 = d->n[1];
+  p->n3 = is3d ? d->n[2] : 1;
+  p->B = d->batch;
+  p->C = d->ncomp;
+  p->kin = d->kinetics;
+  p->P = d->nparams;
+  p->tau = d->tau;
+  p->npts = (long long)p->n1 * p->n2 * p->n3;
+  p->elems = p->npts * p->B * p->C;
+
+  int rc = CG_OK;
+  auto bail = [&](int code) {
+    cg_plan_destroy(p);
+    return code;
+  };
+  const int C = p->C;
+  if ((rc = upload(p, d->coeff, C, &p->coeff))) return bail(rc);
+  if ((rc = upload(p, d->lift, C, &p->lift))) return bail(rc);
+  if (d->kin_params && d->nparams > 0) {
+    if ((rc = upload(p, d->kin_params, (size_t)p->B * d->nparams, &p->kin_params))) return bail(rc);
+  } else if (p->kin != CG_KIN_EXTERNAL) {
+    return bail(fail(CG_EINVAL, "kinetics parameters missing"));
+  }
+  if (!d->theta_stencil) return bail(fail(CG_EINVAL, "theta stencil missing"));
+  if ((rc = upload(p, d->theta_stencil, 2 * (size_t)C, &p->th))) return bail(rc);
+  int n_rho = 0, n_phi = 0, n_z = 0;
+  if (p->geom == CG_DISK) n_rho = p->n1;
+  if (p->geom == CG_SPHERE) n_phi = p->n2;
+  if (p->geom == CG_BALL) {
+    n_rho = p->n1;
+    n_phi = p->n3;
+  }
+  if (p->geom == CG_CYLINDER) {
+    n_rho = p->n1;
+    n_z = p->n3;
+  }
+  if (n_rho) {
+    if (!d->rho_bands || !d->d_rho) return bail(fail(CG_EINVAL, "rho operator missing"));
+    if ((rc = bands_upload(p, d->rho_bands, n_rho, &p->rho_b))) return bail(rc);
+    if ((rc = upload(p, d->d_rho, (size_t)C * n_rho, &p->d_rho))) return bail(rc);
+  }
+  if (n_phi) {
+    if (!d->phi_bands || !d->d_phi) return bail(fail(CG_EINVAL, "phi operator missing"));
+    if ((rc = bands_upload(p, d->phi_bands, n_phi, &p->phi_b))) return bail(rc);
+    if ((rc = upload(p, d->d_phi, (size_t)C * n_phi, &p->d_phi))) return bail(rc);
+  }
+  if (n_z) {
+    if (!d->z_bands) return bail(fail(CG_EINVAL, "z operator missing"));
+    if ((rc = bands_upload(p, d->z_bands, n_z, &p->z_b))) return bail(rc);
+  }
+  if ((rc = build_stages(p, d))) return bail(rc);
+  for (const Stage& st : p->stages) {
+    CUtensorMap dummy{};
+    GemmParams gp{};
+    if ((rc = launch_gemm(st.var, st.epi, st.cfg, dummy, dummy, gp, nullptr, true))) return bail(rc);
+  }
+  const size_t bytes = (size_t)p->elems * sizeof(double);
+  if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&p->X)))) return bail(rc);
+  if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&p->Y)))) return bail(rc);
+  if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&p->S2)))) return bail(rc);
+  if ((rc = dev_alloc(p, sizeof(int), reinterpret_cast<void**>(&p->step_dev)))) return bail(rc);
+  if ((rc = dev_alloc(p, sizeof(int) * (size_t)p->B * C, reinterpret_cast<void**>(&p->scratch_bad))))
+    return bail(rc);
+  cudaError_t e = cudaMemset(p->step_dev, 0, sizeof(int));
+  if (e != cudaSuccess) return bail(fail(CG_ECUDA, cudaGetErrorString(e)));
+  e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return bail(fail(CG_ECUDA, cudaGetErrorString(e)));
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return bail(fail(CG_ECUDA, cudaGetErrorString(e)));
+  *out = p;
+  return CG_OK;
+}
+
+int cg_apply_diffusion(cg_plan* p, const double* W, double* out, void* stream) {
+  if (!p || !W || !out) return fail(CG_EINVAL, "null argument");
+  StencilParams sp{};
+  sp.geometry = p->geom;
+  sp.n1 = p->n1;
+  sp.n2 = p->n2;
+  sp.n3 = p->n3;
+  sp.ncomp = p->C;
+  sp.batch = p->B;
+  sp.npts = p->npts;
+  sp.rho_b = p->rho_b;
+  sp.phi_b = p->phi_b;
+  sp.z_b = p->z_b;
+  sp.th = p->th;
+  sp.d_rho = p->d_rho;
+  sp.d_phi = p->d_phi;
+  sp.coeff = p->coeff;
+  sp.lift = p->lift;
+  sp.W = W;
+  sp.F = out;
+  sp.with_diffusion = 1;
+  sp.with_reaction = 0;
+  return launch_fbuild(p->geom, KIN_EXTERNAL, sp, static_cast<cudaStream_t>(stream));
+}
+
+int cg_kinetics(cg_plan* p, const double* W, double* G, void* stream) {
+  if (!p || !W || !G) return fail(CG_EINVAL, "null argument");
+  if (p->kin == CG_KIN_EXTERNAL) return fail(CG_EINVAL, "plan has no built-in kinetics");
+  StencilParams sp{};
+  sp.geometry = p->geom;
+  sp.n1 = p->n1;
+  sp.n2 = p->n2;
+  sp.n3 = p->n3;
+  sp.ncomp = p->C;
+  sp.batch = p->B;
+  sp.npts = p->npts;
+  sp.lift = p->lift;
+  sp.kin = p->kin_params;
+  sp.nparams = p->P;
+  sp.W = W;
+  sp.F = G;
+  sp.with_diffusion = 0;
+  sp.with_reaction = 1;
+  return launch_fbuild(p->geom, p->kin, sp, static_cast<cudaStream_t>(stream));
+}
+
+int cg_step(cg_plan* p, const double* W, const double* G, double* W_out, void* stream) {
+  if (!p || !W || !G || !W_out) return fail(CG_EINVAL, "null argument");
+  if (W == W_out) return fail(CG_EINVAL, "W_out must not alias W");
+  return launch_step(p, W, W_out, G, false, p->scratch_bad, false, static_cast<cudaStream_t>(stream));
+}
+
+int cg_run(cg_plan* p, double* state, long long step0, long long nsteps, int* first_bad, void* stream) {
+  if (!p || !state || !first_bad) return fail(CG_EINVAL, "null argument");
+  if (nsteps < 0) return fail(CG_EINVAL, "nsteps must be >= 0");
+  if (p->kin == CG_KIN_EXTERNAL) return fail(CG_EINVAL, "cg_run needs built-in kinetics");
+  if (step0 + nsteps > INT_MAX) return fail(CG_EINVAL, "step index overflow");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (nsteps == 0) return CG_OK;
+  set_step_kernel<<<1, 1, 0, s>>>(p->step_dev, (int)step0);
+  CUDA_TRY(cudaGetLastError());
+  int rc;
+  long long done = 0;
+  if (nsteps >= kChunk) {
+    GraphEntry* ge = nullptr;
+    for (auto& g : p->graphs)
+      if (g.state == state && g.first_bad == first_bad) ge = &g;
+    if (!ge) {
+      // capture kChunk steps state -> S2 -> state ... on a private stream
+      CUDA_TRY(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+      int crc = CG_OK;
+      for (int k = 0; k < kChunk && crc == CG_OK; ++k) {
+        const bool even = (k % 2) == 0;
+        crc = launch_step(p, even ? state : p->S2, even ? p->S2 : state, nullptr, true, first_bad, true,
+                          p->cap_stream);
+      }
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaStreamEndCapture(p->cap_stream, &graph);
+      if (crc) {
+        if (graph) cudaGraphDestroy(graph);
+        return crc;
+      }
+      if (e != cudaSuccess) return fail(CG_ECUDA, std::string("capture: ") + cudaGetErrorString(e));
+      cudaGraphExec_t exec = nullptr;
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return fail(CG_ECUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+      if (p->graphs.size() >= 4) {
+        cudaGraphExecDestroy(p->graphs.front().chunk);
+        p->graphs.erase(p->graphs.begin());
+      }
+      p->graphs.push_back(GraphEntry{state, first_bad, exec});
+      ge = &p->graphs.back();
+    }
+    while (nsteps - done >= kChunk) {
+      CUDA_TRY(cudaGraphLaunch(ge->chunk, s));
+      done += kChunk;
+    }
+  }
+  // remainder eagerly, in pairs; an odd last step lands in S2 and is copied back
+  while (done < nsteps) {
+    if ((rc = launch_step(p, state, p->S2, nullptr, true, first_bad, true, s))) return rc;
+    ++done;
+    if (done < nsteps) {
+      if ((rc = launch_step(p, p->S2, state, nullptr, true, first_bad, true, s))) return rc;
+      ++done;
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(state, p->S2, (size_t)p->elems * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  return CG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,146 @@
+"""Ensembles of independent runs (seed / parameter sweeps), batched into one
+plan per GPU and sharded over ranks.
+
+The reference has no parallel path; its docs call runs "embarrassingly
+parallel".  Here rank r of G takes the contiguous runs
+[r R / G, (r+1) R / G); runs never communicate while stepping, and one
+collective at the end gathers the final physical fields to rank 0 (NCCL over
+NVLink on GPUs; gloo in the CPU tests of the gather logic).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .integrators import INT32_MAX, DivergenceError, SplitPlan, engine_kinetics, prepare
+
+
+def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous [start, stop) of `total` runs owned by `rank` of `world`."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return (rank * total) // world, ((rank + 1) * total) // world
+
+
+def gather_fields(local, total: int, group=None, dst: int = 0):
+    """Gather per-rank blocks [n_r, ...] of a [total, ...] array to `dst`.
+
+    Uses torch.distributed.gather on equal-size padded blocks (NCCL needs
+    equal shapes); returns the [total, ...] tensor on dst and None elsewhere.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    biggest = max(shard_range(total, r, world)[1] - shard_range(total, r, world)[0] for r in range(world))
+    pad = torch.zeros((biggest,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    bufs = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
+    dist.gather(pad, bufs, dst=dst, group=group)
+    if rank != dst:
+        return None
+    parts = []
+    for r in range(world):
+        lo, hi = shard_range(total, r, world)
+        parts.append(bufs[r][: hi - lo])
+    return torch.cat(parts, dim=0)
+
+
+def ensemble_plan(template, kin_kind: str, params: np.ndarray, tau: float) -> SplitPlan:
+    """One batched plan: operators from the template system, per-run kinetics
+    parameters ``params`` [B, P]."""
+    geos = [prepare(c.ops, tau) for c in template.components]
+    lifts = [float(getattr(c, "lift", 0.0)) for c in template.components]
+    return SplitPlan(geos, batch=params.shape[0], kinetics=kin_kind, kin_params=params, lifts=lifts)
+
+
+def _check_shared(systems):
+    ref = systems[0]
+    for s in systems[1:]:
+        for a, b in zip(ref.components, s.components):
+            if a.name != b.name or a.ops is not b.ops and not _same_ops(a.ops, b.ops) or a.lift != b.lift:
+                raise NotImplementedError("ensemble members must share operators, coefficients and lifts")
+        if engine_kinetics(s).kind != engine_kinetics(ref).kind:
+            raise NotImplementedError("ensemble members must share the kinetics kind")
+
+
+def _same_ops(x, y) -> bool:
+    if x.coeff != y.coeff or str(x.geometry) != str(y.geometry):
+        return False
+    for axis in ("rho", "theta", "phi", "z"):
+        p, q = getattr(x, axis), getattr(y, axis)
+        if (p is None) != (q is None):
+            return False
+        if p is None:
+            continue
+        for attr in ("a", "b", "c", "grid", "diag", "off"):
+            u, v = getattr(p, attr, None), getattr(q, attr, None)
+            if not np.array_equal(np.asarray(u), np.asarray(v)):
+                return False
+    wx, wy = getattr(x, "rho_weights", None), getattr(y, "rho_weights", None)
+    if (wx is None) != (wy is None):
+        return False
+    return wx is None or np.array_equal(wx.values, wy.values)
+
+
+@dataclass
+class EnsembleResult:
+    fields: object  # [R, C, ...] physical fields on rank 0 (numpy or torch), None elsewhere
+    first_bad: np.ndarray  # [n_local, C] first diverged step (INT32_MAX = never), this rank's runs
+    start: int
+    stop: int
+    steps: int
+    tau: float
+
+
+def run_ensemble(systems, m: int, t_star: float, *, group=None, gather: bool = True,
+                 as_torch: bool = False, raise_on_divergence: bool = False) -> EnsembleResult:
+    """Advance every member of ``systems`` (a list of CoupledSystem sharing
+    operators) by m steps of tau = t*/m; shard over the torch.distributed
+    group when one is initialised."""
+    import torch
+    import torch.distributed as dist
+
+    if m < 1:
+        raise ValueError("need at least one time step")
+    if t_star <= 0:
+        raise ValueError("t_star must be positive")
+    R = len(systems)
+    if R == 0:
+        raise ValueError("empty ensemble")
+    dist_on = dist.is_available() and dist.is_initialized()
+    world = dist.get_world_size(group) if dist_on else 1
+    rank = dist.get_rank(group) if dist_on else 0
+    lo, hi = shard_range(R, rank, world)
+    mine = systems[lo:hi]
+    tau = t_star / m
+    if mine:
+        _check_shared(mine)
+        kin = engine_kinetics(mine[0])
+        params = np.stack([engine_kinetics(s).param_vector() for s in mine])
+        plan = ensemble_plan(mine[0], kin.kind, params, tau)
+        host = np.stack([np.stack([np.asarray(c.initial, dtype=np.float64) for c in s.components]) for s in mine])
+        state = torch.from_numpy(np.ascontiguousarray(host)).to("cuda")
+        first_bad = torch.full((hi - lo, plan.ncomp), INT32_MAX, dtype=torch.int32, device="cuda")
+        plan.run(state, 0, m, first_bad)
+        lifts = torch.tensor([float(getattr(c, "lift", 0.0)) for c in mine[0].components],
+                             dtype=torch.float64, device="cuda")
+        phys = state + lifts.view((1, -1) + (1,) * (state.dim() - 2))
+        bad = first_bad.cpu().numpy()
+    else:
+        shape = tuple(systems[0].components[0].ops.shape)
+        phys = torch.zeros((0, len(systems[0].components)) + shape, dtype=torch.float64, device="cuda")
+        bad = np.zeros((0, len(systems[0].components)), dtype=np.int32)
+    if raise_on_divergence and bad.size and bad.min() < INT32_MAX:
+        s = int(bad.min())
+        raise DivergenceError(f"ensemble run diverged at step {s}", step=s)
+    if dist_on and gather and world > 1:
+        full = gather_fields(phys, R, group=group)
+    else:
+        full = phys if rank == 0 else None
+    if full is not None and not as_torch:
+        full = full.cpu().numpy()
+    return EnsembleResult(full, bad, lo, hi, m, tau)

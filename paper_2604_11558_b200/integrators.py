@@ -1,0 +1,539 @@
+"""Drop-in split exponential Euler engine on the B200.
+
+Public surface mirrors the reference module ``curvipat.integrators``
+(integrators.py): ``Geometry``, ``ComponentOps``, ``GeometryOps``,
+``prepare``, ``apply_diffusion``, ``step_split``, ``STEPPERS``,
+``run_simulation``, ``RunResult``, ``DivergenceError``,
+``DIVERGENCE_LIMIT``.  ``prepare`` stays a host computation (north_star:
+"operator assembly and the one-off phi1 evaluation ... may stay on the
+host"); everything per step runs in libcurvigpu.so:
+
+    apply_diffusion  -> cg_apply_diffusion (stencil kernel)
+    step_split       -> cg_step            (F kernel + DMMA GEMM chain)
+    run_simulation   -> cg_run             (CUDA-graph time loop, fused
+                                             kinetics, on-device guard)
+
+There is no CPU path: without a CUDA device or the built library these
+functions raise.  Inputs are never mutated; numpy in -> numpy out, torch in
+-> torch out (same device).  All work is ordered on the caller's current
+torch CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from enum import Enum
+from typing import Callable
+
+import numpy as np
+
+from . import _native
+from .operators import (
+    DiagonalWeights,
+    EigenFactorization,
+    PeriodicTridiagonal,
+    TridiagonalOperator,
+    eig_theta,
+    eig_tridiag,
+)
+from .phifun import PhiTensor, phi1_matrix, phi1_outer
+
+DIVERGENCE_LIMIT = 1e12  # integrators.py:33
+INT32_MAX = 2**31 - 1
+
+
+class DivergenceError(RuntimeError):
+    """A field left the finite range; ``step`` is the 1-based step index
+    (integrators.py:37-43)."""
+
+    def __init__(self, message: str, step: int):
+        super().__init__(message)
+        self.step = step
+
+
+class Geometry(Enum):
+    DISK = "disk"
+    SPHERE = "sphere"
+    BALL = "ball"
+    CYLINDER = "cylinder"
+
+
+def _geometry_name(g) -> str:
+    """Accept our Geometry, the reference's Geometry enum, or a string."""
+    return g.value if isinstance(g, Enum) else str(g)
+
+
+@dataclass(frozen=True)
+class ComponentOps:
+    """Geometry tag, diffusion coefficient and the 1-D operators of one
+    component (integrators.py:53-84).  Reference ComponentOps objects are
+    accepted everywhere this type is."""
+
+    geometry: Geometry
+    coeff: float
+    rho: TridiagonalOperator | None = None
+    theta: PeriodicTridiagonal | None = None
+    phi: TridiagonalOperator | None = None
+    z: TridiagonalOperator | None = None
+    rho_weights: DiagonalWeights | None = None
+
+    @property
+    def shape(self) -> tuple[int, ...]:
+        return _shape_of(self)
+
+    def rho_weight_values(self):
+        if self.rho is None:
+            return None
+        if self.rho_weights is not None:
+            return self.rho_weights.values
+        return self.rho.grid**-2.0
+
+
+def _shape_of(base) -> tuple[int, ...]:
+    g = _geometry_name(base.geometry)
+    if g == "disk":
+        return (base.rho.n, base.theta.n)
+    if g == "sphere":
+        return (base.theta.n, base.phi.n)
+    if g == "ball":
+        return (base.rho.n, base.theta.n, base.phi.n)
+    return (base.rho.n, base.theta.n, base.z.n)
+
+
+@dataclass(frozen=True)
+class GeometryOps:
+    """Per-(component, tau) operands built once by :func:`prepare`
+    (integrators.py:87-127); host arrays, uploaded into a plan."""
+
+    base: object
+    tau: float
+    A_rho: np.ndarray | None = None
+    A_theta: np.ndarray | None = None
+    A_phi: np.ndarray | None = None
+    A_z: np.ndarray | None = None
+    d_rho: np.ndarray | None = None
+    d_phi: np.ndarray | None = None
+    Q_theta: np.ndarray | None = None
+    lam_theta: np.ndarray | None = None
+    phi_fac: EigenFactorization | None = None
+    phi_mix: PhiTensor | None = None
+    phi_mix_outer: PhiTensor | None = None
+    phi1_rho: np.ndarray | None = None
+    phi1_phi: np.ndarray | None = None
+    phi1_z: np.ndarray | None = None
+
+    @property
+    def geometry(self):
+        return self.base.geometry
+
+    @property
+    def coeff(self) -> float:
+        return self.base.coeff
+
+    @property
+    def shape(self) -> tuple[int, ...]:
+        return _shape_of(self.base)
+
+
+def _rho_weights(base):
+    if base.rho is None:
+        return None
+    w = getattr(base, "rho_weights", None)
+    if w is not None:
+        return np.asarray(w.values, dtype=float)
+    return base.rho.grid**-2.0
+
+
+def prepare(base, tau: float) -> GeometryOps:
+    """Host setup of every transform and phi1 factor for one component at a
+    fixed step (integrators.py:130-173).  Dense A_* copies are kept for API
+    parity; the engine applies the stencils from the bands."""
+    if tau < 0:
+        raise ValueError("tau must be nonnegative")
+    g = _geometry_name(base.geometry)
+    s = tau * base.coeff
+    kw: dict = {}
+    if base.theta is not None:
+        fac = eig_theta(base.theta)
+        kw.update(A_theta=base.theta.toarray(), Q_theta=fac.Q, lam_theta=fac.lambdas)
+    if base.rho is not None:
+        kw.update(A_rho=base.rho.toarray(), d_rho=_rho_weights(base),
+                  phi1_rho=phi1_matrix(s, eig_tridiag(base.rho)))
+    if base.phi is not None:
+        fac = eig_tridiag(base.phi)
+        kw.update(A_phi=base.phi.toarray(), d_phi=np.sin(base.phi.grid) ** -2.0, phi_fac=fac)
+        if g == "sphere":
+            kw["phi1_phi"] = phi1_matrix(s, fac)
+    if base.z is not None:
+        kw.update(A_z=base.z.toarray(), phi1_z=phi1_matrix(s, eig_tridiag(base.z)))
+    if g == "disk":
+        kw["phi_mix"] = phi1_outer(s, [kw["d_rho"], kw["lam_theta"]])
+    elif g == "sphere":
+        kw["phi_mix"] = phi1_outer(s, [kw["lam_theta"], kw["d_phi"]])
+    elif g == "ball":
+        kw["phi_mix_outer"] = phi1_outer(s, [kw["d_rho"], np.ones(base.theta.n), kw["phi_fac"].lambdas])
+        kw["phi_mix"] = phi1_outer(s, [kw["d_rho"], kw["lam_theta"], kw["d_phi"]])
+    elif g == "cylinder":
+        kw["phi_mix"] = phi1_outer(s, [kw["d_rho"], kw["lam_theta"], np.ones(base.z.n)])
+    else:
+        raise ValueError(f"unknown geometry {g!r}")
+    return GeometryOps(base=base, tau=tau, **kw)
+
+
+# ---------------------------------------------------------------------------
+# plan: host operands -> libcurvigpu
+# ---------------------------------------------------------------------------
+
+KINETICS_CODES = {
+    "external": 0,
+    "schnakenberg": 1,
+    "brusselator": 2,
+    "gray_scott": 3,
+    "bvam_eta": 4,
+    "bvam": 5,
+    "dib": 6,
+}
+
+
+def _f64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _bands(op) -> np.ndarray:
+    out = np.zeros((3, op.n))
+    out[0] = op.a
+    out[1, :-1] = op.b
+    out[2, :-1] = op.c
+    return out
+
+
+class SplitPlan:
+    """A libcurvigpu plan for ``batch`` runs of a ``len(geos)``-component
+    system whose components share geometry and grid.
+
+    State tensors are torch.float64 CUDA tensors of shape
+    ``(batch, ncomp, *grid)``, C-contiguous, reference axis order.
+    """
+
+    def __init__(self, geos, batch: int = 1, kinetics: str = "external",
+                 kin_params=None, lifts=None):
+        import torch  # noqa: F401  (device memory / streams)
+
+        geos = list(geos)
+        if not geos:
+            raise ValueError("need at least one component")
+        g = _geometry_name(geos[0].geometry)
+        shape = tuple(geos[0].shape)
+        taus = {float(o.tau) for o in geos}
+        if any(_geometry_name(o.geometry) != g or tuple(o.shape) != shape for o in geos):
+            raise NotImplementedError("components of one plan must share geometry and grid "
+                                      "(mixed bulk-surface systems are out of scope)")
+        if len(taus) != 1:
+            raise ValueError("components must share tau")
+        if kinetics not in KINETICS_CODES:
+            raise NotImplementedError(f"kinetics {kinetics!r} has no GPU kernel")
+        self.geometry = g
+        self.shape = shape
+        self.batch = int(batch)
+        self.ncomp = len(geos)
+        self.tau = taus.pop()
+        C = self.ncomp
+        keep = {}
+
+        def stack(fn):
+            arr = _f64(np.stack([fn(o) for o in geos]))
+            keep[id(arr)] = arr
+            return arr
+
+        d = _native.cg_desc()
+        d.geometry = _native.GEOMETRY_CODES[g]
+        n = list(shape) + [1] * (3 - len(shape))
+        d.n[0], d.n[1], d.n[2] = n
+        d.batch = self.batch
+        d.ncomp = C
+        d.tau = self.tau
+        coeff = stack(lambda o: o.coeff)
+        d.coeff = _native.dptr(coeff)
+        lift = _f64(np.zeros(C) if lifts is None else np.asarray(lifts, dtype=float))
+        keep[id(lift)] = lift
+        d.lift = _native.dptr(lift)
+        base0 = geos[0].base
+        if base0.theta is not None:
+            d.theta_stencil = _native.dptr(stack(lambda o: [o.base.theta.diag, o.base.theta.off]))
+            d.Q_theta = _native.dptr(stack(lambda o: o.Q_theta))
+        if base0.rho is not None:
+            d.rho_bands = _native.dptr(stack(lambda o: _bands(o.base.rho)))
+            d.d_rho = _native.dptr(stack(lambda o: o.d_rho))
+            d.phi1_rho = _native.dptr(stack(lambda o: o.phi1_rho))
+        if base0.phi is not None:
+            d.phi_bands = _native.dptr(stack(lambda o: _bands(o.base.phi)))
+            d.d_phi = _native.dptr(stack(lambda o: o.d_phi))
+        if base0.z is not None:
+            d.z_bands = _native.dptr(stack(lambda o: _bands(o.base.z)))
+            d.phi1_z = _native.dptr(stack(lambda o: o.phi1_z))
+        if g == "sphere":
+            d.phi1_phi = _native.dptr(stack(lambda o: o.phi1_phi))
+        if g == "ball":
+            d.V_phi = _native.dptr(stack(lambda o: o.phi_fac.V))
+            d.Vinv_phi = _native.dptr(stack(lambda o: o.phi_fac.V_inv))
+            d.Phi_outer = _native.dptr(stack(lambda o: o.phi_mix_outer.field[:, 0, :]))
+            d.Phi = _native.dptr(stack(lambda o: o.phi_mix.field))
+        elif g == "cylinder":
+            d.Phi = _native.dptr(stack(lambda o: o.phi_mix.field[:, :, 0]))
+        else:
+            d.Phi = _native.dptr(stack(lambda o: o.phi_mix.field))
+        d.kinetics = KINETICS_CODES[kinetics]
+        self.kinetics = kinetics
+        if kin_params is not None:
+            kp = _f64(kin_params).reshape(self.batch, -1)
+            keep[id(kp)] = kp
+            d.nparams = kp.shape[1]
+            d.kin_params = _native.dptr(kp)
+        self._lib = _native.lib()
+        handle = ctypes.c_void_p()
+        _native.check(self._lib.cg_plan_create(ctypes.byref(d), ctypes.byref(handle)), "cg_plan_create")
+        self._h = handle
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.cg_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- helpers -------------------------------------------------------------
+    @property
+    def state_shape(self):
+        return (self.batch, self.ncomp) + self.shape
+
+    def _check_state(self, t, name):
+        import torch
+
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
+            raise ValueError(f"{name} must be a CUDA float64 tensor")
+        if tuple(t.shape) != self.state_shape or not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous with shape {self.state_shape}, got {tuple(t.shape)}")
+
+    @staticmethod
+    def _stream():
+        import torch
+
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    # -- entry points --------------------------------------------------------
+    def apply_diffusion(self, W, out):
+        self._check_state(W, "W")
+        self._check_state(out, "out")
+        _native.check(self._lib.cg_apply_diffusion(self._h, W.data_ptr(), out.data_ptr(), self._stream()),
+                      "cg_apply_diffusion")
+
+    def kinetics_into(self, W, G):
+        self._check_state(W, "W")
+        self._check_state(G, "G")
+        _native.check(self._lib.cg_kinetics(self._h, W.data_ptr(), G.data_ptr(), self._stream()), "cg_kinetics")
+
+    def step(self, W, G, out):
+        self._check_state(W, "W")
+        self._check_state(G, "G")
+        self._check_state(out, "out")
+        _native.check(self._lib.cg_step(self._h, W.data_ptr(), G.data_ptr(), out.data_ptr(), self._stream()),
+                      "cg_step")
+
+    def run(self, state, step0: int, nsteps: int, first_bad):
+        """Advance ``state`` in place; ``first_bad`` is an int32 CUDA tensor
+        of shape (batch, ncomp) receiving the first diverged step per field."""
+        import torch
+
+        self._check_state(state, "state")
+        if first_bad.dtype != torch.int32 or not first_bad.is_cuda or first_bad.numel() != self.batch * self.ncomp:
+            raise ValueError("first_bad must be an int32 CUDA tensor with batch*ncomp entries")
+        _native.check(self._lib.cg_run(self._h, state.data_ptr(), int(step0), int(nsteps), first_bad.data_ptr(),
+                                       self._stream()), "cg_run")
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped entry points
+# ---------------------------------------------------------------------------
+
+_PLAN_CACHE: dict[int, tuple[object, SplitPlan]] = {}
+
+
+def _plan_for(ops) -> SplitPlan:
+    hit = _PLAN_CACHE.get(id(ops))
+    if hit is not None and hit[0] is ops:
+        return hit[1]
+    plan = SplitPlan([ops], batch=1)
+    if len(_PLAN_CACHE) > 64:
+        _PLAN_CACHE.clear()
+    _PLAN_CACHE[id(ops)] = (ops, plan)
+    return plan
+
+
+def _to_device(x, shape):
+    import torch
+
+    if isinstance(x, torch.Tensor):
+        if tuple(x.shape) != tuple(shape):
+            raise ValueError(f"field shape {tuple(x.shape)} does not match {tuple(shape)}")
+        return x.to(device="cuda", dtype=torch.float64).contiguous().reshape((1, 1) + tuple(shape)), True
+    arr = np.asarray(x, dtype=np.float64)
+    if arr.shape != tuple(shape):
+        raise ValueError(f"field shape {arr.shape} does not match {tuple(shape)}")
+    return torch.from_numpy(np.ascontiguousarray(arr)).to("cuda").reshape((1, 1) + tuple(shape)), False
+
+
+def _from_device(t, shape, as_torch, like=None):
+    out = t.reshape(tuple(shape))
+    if as_torch:
+        return out if like is None else out.to(like.device)
+    return out.cpu().numpy()
+
+
+def apply_diffusion(ops: GeometryOps, W):
+    """coeff * M W on the GPU (integrators.py:176-199)."""
+    import torch
+
+    plan = _plan_for(ops)
+    Wd, is_t = _to_device(W, ops.shape)
+    out = torch.empty_like(Wd)
+    plan.apply_diffusion(Wd, out)
+    return _from_device(out, ops.shape, is_t, W if is_t else None)
+
+
+def step_split(ops: GeometryOps, W, G):
+    """One split exponential Euler step on the GPU (integrators.py:247-249)."""
+    import torch
+
+    plan = _plan_for(ops)
+    Wd, is_t = _to_device(W, ops.shape)
+    Gd, _ = _to_device(G, ops.shape)
+    out = torch.empty_like(Wd)
+    plan.step(Wd, Gd, out)
+    return _from_device(out, ops.shape, is_t, W if is_t else None)
+
+
+def _geometry_stepper(name):
+    def stepper(ops, W, G):
+        if _geometry_name(ops.geometry) != name:
+            raise ValueError(f"{name} stepper got a {_geometry_name(ops.geometry)} operator")
+        return step_split(ops, W, G)
+
+    stepper.__name__ = f"step_split_{name}"
+    return stepper
+
+
+step_split_disk = _geometry_stepper("disk")
+step_split_sphere = _geometry_stepper("sphere")
+step_split_ball = _geometry_stepper("ball")
+step_split_cylinder = _geometry_stepper("cylinder")
+
+STEPPERS: dict[Geometry, Callable] = {
+    Geometry.DISK: step_split_disk,
+    Geometry.SPHERE: step_split_sphere,
+    Geometry.BALL: step_split_ball,
+    Geometry.CYLINDER: step_split_cylinder,
+}
+
+
+@dataclass
+class RunResult:
+    """Final (lifted) fields plus the sampled series (integrators.py:359-367)."""
+
+    fields: dict
+    times: list = field(default_factory=list)
+    series: dict = field(default_factory=dict)
+    steps: int = 0
+    tau: float = 0.0
+
+
+def engine_kinetics(system):
+    """The GPU kinetics descriptor of a system, or NotImplementedError for an
+    arbitrary Python closure (it cannot run on the device)."""
+    from .models import Kinetics
+
+    kin = getattr(system, "kinetics", None)
+    if isinstance(kin, Kinetics):
+        return kin
+    kin = getattr(system, "engine_kinetics", None)
+    if isinstance(kin, Kinetics):
+        return kin
+    raise NotImplementedError(
+        "system.kinetics is an arbitrary Python callable; the B200 engine needs a "
+        "paper_2604_11558_b200.models.Kinetics descriptor (no CPU fallback)")
+
+
+def run_simulation(system, m: int, t_star: float, *, record_every: int | None = None,
+                   diagnostics: Callable | None = None, sample_hook: Callable | None = None,
+                   method: str = "split", as_torch: bool = False) -> RunResult:
+    """GPU run of a coupled system (integrators.py:370-430).
+
+    Kinetics are evaluated from the common state before any component is
+    updated; samples are taken at step 0, every ``record_every`` steps and at
+    the final step (host copies only there); the divergence guard runs on the
+    device after every step and raises ``DivergenceError(step)`` naming the
+    first bad step and component, as the reference does.
+    """
+    import torch
+
+    if m < 1:
+        raise ValueError("need at least one time step")
+    if t_star <= 0:
+        raise ValueError("t_star must be positive")
+    if method not in ("split", "forward_euler"):
+        raise ValueError(f"unknown method {method!r}")
+    if method != "split":
+        raise NotImplementedError("forward Euler is a reference comparison path, not part of the engine")
+    kin = engine_kinetics(system)
+    tau = t_star / m
+    comps = list(system.components)
+    names = [c.name for c in comps]
+    geos = [prepare(c.ops, tau) for c in comps]
+    lifts = [float(getattr(c, "lift", 0.0)) for c in comps]
+    plan = SplitPlan(geos, batch=1, kinetics=kin.kind, kin_params=kin.param_vector()[None, :], lifts=lifts)
+    state = torch.from_numpy(np.ascontiguousarray(np.stack([np.asarray(c.initial, dtype=np.float64)
+                                                            for c in comps]))).to("cuda")
+    state = state.reshape(plan.state_shape).contiguous()
+    first_bad = torch.full((1, len(comps)), INT32_MAX, dtype=torch.int32, device="cuda")
+    every = record_every or m
+    times: list[float] = []
+    series: dict[str, list[float]] = {n: [] for n in names}
+
+    def host_states():
+        host = state[0].cpu().numpy()
+        return {n: host[i].copy() for i, n in enumerate(names)}
+
+    def take_sample(step):
+        t = step * tau
+        times.append(t)
+        if diagnostics is None and sample_hook is None:
+            return
+        st = host_states()
+        if diagnostics is not None:
+            for name, value in diagnostics(st).items():
+                series[name].append(value)
+        if sample_hook is not None:
+            sample_hook(step, t, st)
+
+    take_sample(0)
+    step = 0
+    while step < m:
+        nxt = min(m, (step // every + 1) * every)
+        plan.run(state, step, nxt - step, first_bad)
+        bad = first_bad.cpu().numpy()[0]
+        if bad.min() < INT32_MAX:
+            s = int(bad.min())
+            c = int(np.flatnonzero(bad == s)[0])
+            raise DivergenceError(f"component {names[c]!r} diverged at step {s}", step=s)
+        step = nxt
+        if step % every == 0 or step == m:
+            take_sample(step)
+    if as_torch:
+        fields = {n: state[0, i].clone() for i, n in enumerate(names)}
+    else:
+        fields = host_states()
+    return RunResult(fields=fields, times=times, series=series, steps=m, tau=tau)

@@ -1,0 +1,279 @@
+"""Systems for the engine: seeded initial fields, GPU kinetics descriptors,
+and the reference's own disk/sphere models.
+
+Mirrors the hot-path half of ``curvipat.models`` (models.py):
+``Xoshiro256pp``/``Uniform``/``Normal`` (bit-exact, backed by C in
+libcurvigpu.so), ``SystemComponent``, ``CoupledSystem``, ``model_spec``,
+``build_system``, ``random_initial_condition``.  The reference's kinetics are
+arbitrary Python closures (models.py:386-391); the engine instead takes a
+:class:`Kinetics` descriptor naming one of the pointwise reactions compiled
+into the F-build kernel.  Bulk-surface models (models.py:322-369, :570-661)
+are out of scope (SURVEY 8(f) "next") and raise NotImplementedError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+
+from . import _native
+from .integrators import ComponentOps, Geometry
+from .operators import DiagonalWeights, build_lambda, build_phi_op, build_rho, build_theta
+
+# ---------------------------------------------------------------------------
+# seeded random numbers (models.py:43-130), C-backed
+# ---------------------------------------------------------------------------
+
+
+class Xoshiro256pp:
+    """xoshiro256++ seeded by splitmix64; same stream as the reference."""
+
+    def __init__(self, seed: int):
+        self._state = (ctypes.c_uint64 * 4)()
+        _native.lib().cg_rng_seed(ctypes.c_uint64(seed & (2**64 - 1)), self._state)
+
+    def next_uint64(self) -> int:
+        out = (ctypes.c_uint64 * 1)()
+        _native.lib().cg_rng_next(self._state, 1, out)
+        return int(out[0])
+
+    def raw(self, size: int) -> np.ndarray:
+        out = np.empty(size, dtype=np.uint64)
+        _native.lib().cg_rng_next(self._state, size, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+        return out
+
+    def uniform(self, size: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
+        out = np.empty(size)
+        _native.lib().cg_rng_uniform(self._state, size, lo, hi, _native.dptr(out))
+        return out
+
+    def normal(self, size: int, sigma: float = 1.0) -> np.ndarray:
+        out = np.empty(size)
+        _native.lib().cg_rng_normal(self._state, size, sigma, _native.dptr(out))
+        return out
+
+
+@dataclass(frozen=True)
+class Uniform:
+    lo: float
+    hi: float
+
+    @property
+    def scale(self) -> float:
+        return (self.hi - self.lo) / math.sqrt(12.0)
+
+    def draw(self, rng: Xoshiro256pp, size: int) -> np.ndarray:
+        return rng.uniform(size, self.lo, self.hi)
+
+
+@dataclass(frozen=True)
+class Normal:
+    sigma: float
+
+    @property
+    def scale(self) -> float:
+        return self.sigma
+
+    def draw(self, rng: Xoshiro256pp, size: int) -> np.ndarray:
+        return rng.normal(size, self.sigma)
+
+
+def unvec(w, dims):
+    """First-index-fastest unflattening (tensor.py:24-28)."""
+    return np.asarray(w).reshape(dims, order="F")
+
+
+# ---------------------------------------------------------------------------
+# kinetics descriptors
+# ---------------------------------------------------------------------------
+
+KINETICS_PARAMS = {
+    "schnakenberg": ("gamma", "a", "b"),
+    "brusselator": ("A", "B"),
+    "gray_scott": ("F", "k"),
+    "bvam_eta": ("eta", "a", "b", "h", "C"),
+    "bvam": ("alpha1", "alpha2", "alpha3", "beta1", "beta2"),
+    "dib": ("zeta1", "zeta2", "zeta3", "zeta4", "zeta5", "eta1", "eta2", "eta3", "eta5"),
+}
+
+
+@dataclass(frozen=True)
+class Kinetics:
+    """A pointwise two-species reaction the F-build kernel evaluates on the
+    physical fields (lifted state + lift):
+
+    - ``schnakenberg``: gamma(a - u + u^2 v), gamma(b - u^2 v)
+      (models.py:293-296 scaled by alpha1 as in :528-532)
+    - ``brusselator``: A - (B+1)u + u^2 v, B u - u^2 v
+    - ``gray_scott``: -u v^2 + F(1-u), u v^2 - (F+k) v
+    - ``bvam_eta``: eta(u + a v - C u v - u v^2), eta(b v + h u + C u v + u v^2)
+    - ``bvam``: models.py:284-290
+    - ``dib``: zeta1 * models.py:311-319 with eta4 from :299-308
+    """
+
+    kind: str
+    params: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        if self.kind not in KINETICS_PARAMS:
+            raise NotImplementedError(f"no GPU kernel for kinetics {self.kind!r}")
+        missing = [k for k in KINETICS_PARAMS[self.kind] if k not in self.params]
+        if missing:
+            raise ValueError(f"{self.kind} kinetics missing parameters {missing}")
+
+    def param_vector(self) -> np.ndarray:
+        return np.array([float(self.params[k]) for k in KINETICS_PARAMS[self.kind]])
+
+
+# ---------------------------------------------------------------------------
+# systems
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class SystemComponent:
+    """models.py:377-384."""
+
+    name: str
+    ops: object
+    initial: np.ndarray
+    lift: float = 0.0
+    perturbation: object = None
+
+
+@dataclass(frozen=True)
+class CoupledSystem:
+    """models.py:386-396, with ``kinetics`` a :class:`Kinetics` descriptor."""
+
+    spec: object
+    components: list
+    kinetics: Kinetics
+    equilibrium: dict
+
+    def physical_fields(self, states):
+        lifts = {c.name: c.lift for c in self.components}
+        return {name: W + lifts[name] for name, W in states.items()}
+
+
+class ModelName(Enum):
+    BVAM_DISK = "bvam_disk"
+    SCHNAKENBERG_ANOMALOUS_DISK = "schnakenberg_anomalous_disk"
+    DIB_SPHERE = "dib_sphere"
+    BULK_SURFACE_SCHNAKENBERG_BALL = "bulk_surface_schnakenberg_ball"
+    BSDIB_CYLINDER = "bsdib_cylinder"
+
+
+# published defaults of the three single-geometry models (models.py:148-178)
+_DEFAULTS = {
+    ModelName.BVAM_DISK: ({"gamma": 3.87e-3, "delta": 7.5e-3, "alpha1": 0.899, "alpha2": 0.2,
+                           "alpha3": 0.2, "beta1": -0.91, "beta2": -0.899}, {"rho_star": 1.0}),
+    ModelName.SCHNAKENBERG_ANOMALOUS_DISK: ({"alpha1": 5.0e2, "alpha2": 1.4e-1, "beta1": 1.34,
+                                             "delta": 5.0e1, "lambda": -1.95}, {"rho_star": 1.0}),
+    ModelName.DIB_SPHERE: ({"zeta1": 10.0, "zeta2": 10.0, "zeta3": 1.0, "zeta4": 48.0, "zeta5": 0.5,
+                            "eta1": 5.0, "eta2": 2.5, "eta3": 0.2, "eta5": 1.5, "epsilon": 20.0},
+                           {"rho_star": 1.1653}),
+}
+
+
+@dataclass(frozen=True)
+class ModelSpec:
+    name: ModelName
+    params: dict
+    sizes: dict
+    perturbations: dict
+
+    def equilibrium(self) -> dict:
+        p = self.params
+        if self.name is ModelName.BVAM_DISK:
+            return {"u": 0.0, "v": 0.0}
+        if self.name is ModelName.SCHNAKENBERG_ANOMALOUS_DISK:
+            ue = p["alpha2"] + p["beta1"]
+            return {"u": ue, "v": p["beta1"] / ue**2}
+        if self.name is ModelName.DIB_SPHERE:
+            return {"r": 0.0, "s": p["zeta5"]}
+        raise NotImplementedError(f"{self.name.value} is a bulk-surface model (out of scope)")
+
+
+def model_spec(name, overrides=None) -> ModelSpec:
+    """models.py:247-276 for the single-geometry models."""
+    name = ModelName(name) if isinstance(name, str) else name
+    if name not in _DEFAULTS:
+        raise NotImplementedError(f"{name.value} is a bulk-surface model (out of scope, SURVEY 8(f))")
+    params, sizes = (dict(x) for x in _DEFAULTS[name])
+    for key, value in (overrides or {}).items():
+        if key in sizes:
+            sizes[key] = float(value)
+        elif key in params:
+            params[key] = float(value)
+        else:
+            raise KeyError(f"unknown parameter {key!r} for model {name.value}")
+    if name is ModelName.BVAM_DISK:
+        perts = {"u": Uniform(-0.5, 0.5), "v": Uniform(-0.5, 0.5)}
+    elif name is ModelName.SCHNAKENBERG_ANOMALOUS_DISK:
+        perts = {"u": Normal(1e-5), "v": Normal(1e-5)}
+    else:
+        perts = {"r": Normal(1e-6), "s": Normal(1e-6)}
+    return ModelSpec(name, params, sizes, perts)
+
+
+def random_initial_condition(spec: ModelSpec, seed: int, dims: dict) -> dict:
+    """Equilibrium + seeded perturbation, one generator, component-major, F
+    order (models.py:412-432)."""
+    rng = Xoshiro256pp(seed)
+    if spec.name is ModelName.DIB_SPHERE:
+        shape = (dims["n_theta"], dims["n_phi"])
+    else:
+        shape = (dims["n_rho"], dims["n_theta"])
+    eq = spec.equilibrium()
+    out = {}
+    for name in eq:
+        base = np.full(shape, eq[name])
+        law = spec.perturbations[name]
+        if law is not None:
+            base += unvec(law.draw(rng, int(np.prod(shape))), shape)
+        out[name] = base
+    return out
+
+
+def _component(spec, name, ops, init, lift=0.0):
+    return SystemComponent(name, ops, init[name] - lift, lift, spec.perturbations[name])
+
+
+def build_system(spec, dims: dict, seed: int, overrides=None) -> CoupledSystem:
+    """models.py:454-472 for bvam_disk, schnakenberg_anomalous_disk and
+    dib_sphere, with GPU kinetics descriptors instead of closures."""
+    if not isinstance(spec, ModelSpec):
+        spec = model_spec(spec, overrides)
+    elif overrides:
+        raise ValueError("pass overrides via model_spec when supplying a ModelSpec")
+    p = spec.params
+    init = random_initial_condition(spec, seed, dims)
+    eq = spec.equilibrium()
+    if spec.name is ModelName.BVAM_DISK:
+        rho = build_rho(2, dims["n_rho"], spec.sizes["rho_star"])
+        theta = build_theta(dims["n_theta"])
+        make = lambda k: ComponentOps(Geometry.DISK, k, rho=rho, theta=theta)  # noqa: E731
+        comps = [_component(spec, "u", make(p["gamma"]), init), _component(spec, "v", make(p["delta"]), init)]
+        kin = Kinetics("bvam", {k: p[k] for k in KINETICS_PARAMS["bvam"]})
+    elif spec.name is ModelName.SCHNAKENBERG_ANOMALOUS_DISK:
+        lam = p["lambda"]
+        rho = build_lambda(dims["n_rho"], spec.sizes["rho_star"], lam)
+        weights = DiagonalWeights(rho.grid ** (-2.0 - lam))
+        theta = build_theta(dims["n_theta"])
+        make = lambda k: ComponentOps(Geometry.DISK, k, rho=rho, theta=theta, rho_weights=weights)  # noqa: E731
+        comps = [_component(spec, "u", make(1.0), init, eq["u"]),
+                 _component(spec, "v", make(p["delta"]), init, eq["v"])]
+        kin = Kinetics("schnakenberg", {"gamma": p["alpha1"], "a": p["alpha2"], "b": p["beta1"]})
+    else:
+        rs = spec.sizes["rho_star"]
+        theta = build_theta(dims["n_theta"])
+        phi, _ = build_phi_op(dims["n_phi"])
+        make = lambda k: ComponentOps(Geometry.SPHERE, k, theta=theta, phi=phi)  # noqa: E731
+        comps = [_component(spec, "r", make(1.0 / rs**2), init),
+                 _component(spec, "s", make(p["epsilon"] / rs**2), init)]
+        kin = Kinetics("dib", {k: p[k] for k in KINETICS_PARAMS["dib"]})
+    return CoupledSystem(spec=spec, components=comps, kinetics=kin, equilibrium=eq)

@@ -1,0 +1,322 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE
+implementation (read-only at /root/reference/pkg/src) in this container.
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Outputs (committed; small):
+  rng.json         xoshiro256++ raw / Uniform / Normal streams
+  setup.npz        operator bands, sigma, eigenpairs, phi1 values/tables
+  steps.npz        apply_diffusion and step_split on random fields, all
+                   geometries at small grids (incl. the reference tests' dims)
+  runs.npz         run_simulation of the five BASELINE configs at reduced
+                   grids (physical fields after m steps) + their ICs
+  full.npz         the five BASELINE configs at FULL size: IC checksums and
+                   strided samples / norms of the physical fields after
+                   step 1 and step 100 (config 5: members 0, 255, 511)
+
+The BASELINE systems are built through the reference's public API exactly as
+SURVEY.md Appendix A prescribes (custom kinetics closures for configs 1-4,
+the reference's own schnakenberg_anomalous_disk for config 5).
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import sys
+import time
+from pathlib import Path
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "8")
+import numpy as np  # noqa: E402
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from curvipat import models, tensor  # noqa: E402
+from curvipat import operators as op  # noqa: E402
+from curvipat.integrators import (  # noqa: E402
+    ComponentOps,
+    Geometry,
+    apply_diffusion,
+    prepare,
+    run_simulation,
+    step_split,
+)
+from curvipat.models import CoupledSystem, SystemComponent, Uniform, Xoshiro256pp  # noqa: E402
+from curvipat.phifun import phi1, phi1_matrix, phi1_outer  # noqa: E402
+
+SAMPLES = 4096
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs through the reference API
+# ---------------------------------------------------------------------------
+
+
+def _noise(seed, shape, bases, law):
+    rng = Xoshiro256pp(seed)
+    n = int(np.prod(shape))
+    out = []
+    for b in bases:
+        f = np.full(shape, b)
+        f += tensor.unvec(law.draw(rng, n), shape)
+        out.append(f)
+    return out
+
+
+def z_neumann(n, height):
+    h = height / (n - 1)
+    b = np.full(n - 1, 1.0 / h**2)
+    c = np.full(n - 1, 1.0 / h**2)
+    b[0] = c[-1] = 2.0 / h**2
+    return op.TridiagonalOperator(n=n, a=np.full(n, -2.0 / h**2), b=b, c=c, grid=h * np.arange(n), h=h,
+                                  kind=op.OperatorKind.Z)
+
+
+def ref_config(k, dims, seed=1):
+    spec = models.model_spec("bvam_disk")  # only read by diagnostics
+    if k == 1:
+        n1, n2 = dims
+        rho, th = op.build_rho(2, n1, 1.0), op.build_theta(n2)
+        u0, v0 = _noise(seed, (n1, n2), [1.0, 0.9], Uniform(-1e-3, 1e-3))
+        g, a, b = 100.0, 0.1, 0.9
+
+        def kin(s):
+            u, v = s["u"], s["v"]
+            uuv = u * u * v
+            return {"u": g * (a - u + uuv), "v": g * (b - uuv)}
+
+        comps = [SystemComponent("u", ComponentOps(Geometry.DISK, 1.0, rho=rho, theta=th), u0),
+                 SystemComponent("v", ComponentOps(Geometry.DISK, 10.0, rho=rho, theta=th), v0)]
+    elif k == 2:
+        n1, n2 = dims
+        th = op.build_theta(n1)
+        ph, _ = op.build_phi_op(n2)
+        A, B = 4.5, 6.96
+        u0, v0 = _noise(seed, (n1, n2), [A, B / A], Uniform(-1e-2, 1e-2))
+
+        def kin(s):
+            u, v = s["u"], s["v"]
+            uuv = u * u * v
+            return {"u": A - (B + 1.0) * u + uuv, "v": B * u - uuv}
+
+        comps = [SystemComponent("u", ComponentOps(Geometry.SPHERE, 0.01, theta=th, phi=ph), u0),
+                 SystemComponent("v", ComponentOps(Geometry.SPHERE, 0.08, theta=th, phi=ph), v0)]
+    elif k == 3:
+        n1, n2, n3 = dims
+        rho, th, z = op.build_rho(2, n1, 1.0), op.build_theta(n2), z_neumann(n3, 2.0)
+        rng = Xoshiro256pp(seed)
+        xi = rng.uniform(3)
+        rc, tc, zc = 0.5 * xi[0], 2.0 * np.pi * xi[1], 0.3 + 1.4 * xi[2]
+        n = n1 * n2 * n3
+        eu = tensor.unvec(Uniform(-1.0, 1.0).draw(rng, n), dims)
+        ev = tensor.unvec(Uniform(-1.0, 1.0).draw(rng, n), dims)
+        R, T, Z = np.meshgrid(rho.grid, th.grid, z.grid, indexing="ij")
+        inside = ((np.abs(R * np.cos(T) - rc * np.cos(tc)) <= 0.2)
+                  & (np.abs(R * np.sin(T) - rc * np.sin(tc)) <= 0.2) & (np.abs(Z - zc) <= 0.2))
+        u0 = np.where(inside, 0.5 * (1.0 + 0.01 * eu), 1.0)
+        v0 = np.where(inside, 0.25 * (1.0 + 0.01 * ev), 0.0)
+        F, kk = 0.04, 0.06
+
+        def kin(s):
+            u, v = s["u"], s["v"]
+            uvv = u * v * v
+            return {"u": -uvv + F * (1.0 - u), "v": uvv - (F + kk) * v}
+
+        comps = [SystemComponent("u", ComponentOps(Geometry.CYLINDER, 2e-5, rho=rho, theta=th, z=z), u0),
+                 SystemComponent("v", ComponentOps(Geometry.CYLINDER, 1e-5, rho=rho, theta=th, z=z), v0)]
+    elif k == 4:
+        n1, n2, n3 = dims
+        rho, th = op.build_rho(3, n1, 1.0), op.build_theta(n2)
+        ph, _ = op.build_phi_op(n3)
+        u0, v0 = _noise(seed, dims, [0.0, 0.0], Uniform(-1e-2, 1e-2))
+        eta, a, b, h, C = 0.45, 1.112, -1.01, -1.0, 0.02
+
+        def kin(s):
+            u, v = s["u"], s["v"]
+            uv = u * v
+            uvv = uv * v
+            return {"u": eta * (u + a * v - C * uv - uvv), "v": eta * (b * v + h * u + C * uv + uvv)}
+
+        comps = [SystemComponent("u", ComponentOps(Geometry.BALL, 0.516, rho=rho, theta=th, phi=ph), u0),
+                 SystemComponent("v", ComponentOps(Geometry.BALL, 1.0, rho=rho, theta=th, phi=ph), v0)]
+    else:
+        raise ValueError(k)
+    return CoupledSystem(spec=spec, components=comps, kinetics=kin, equilibrium={})
+
+
+def ref_member(i, dims, runs=512):
+    g = 50.0 + 150.0 * i / (runs - 1)
+    spec = models.model_spec("schnakenberg_anomalous_disk",
+                             {"alpha1": g, "alpha2": 0.1, "beta1": 0.9, "delta": 10.0})
+    return models.build_system(spec, {"n_rho": dims[0], "n_theta": dims[1]}, 1 + i)
+
+
+STEPS = {1: (1000, 1.0), 2: (2000, 2.0), 3: (500, 250.0), 4: (1000, 10.0), 5: (1000, 1.0)}
+FULL = {1: (64, 128), 2: (512, 256), 3: (64, 128, 128), 4: (100, 100, 100), 5: (128, 256)}
+SMALL = {1: (16, 32), 2: (24, 16), 3: (8, 16, 16), 4: (10, 12, 10), 5: (16, 32)}
+
+
+def physical(system, states):
+    return {c.name: states[c.name] + c.lift for c in system.components}
+
+
+# ---------------------------------------------------------------------------
+
+
+def make_rng():
+    out = {}
+    for seed in (0, 1, 123, 2**63 + 5):
+        r = Xoshiro256pp(seed)
+        out[str(seed)] = {
+            "raw": [str(r.next_uint64()) for _ in range(16)],
+            "uniform": Uniform(-1e-3, 1e-3).draw(Xoshiro256pp(seed), 17).tolist(),
+            "normal": models.Normal(1e-5).draw(Xoshiro256pp(seed), 17).tolist(),
+        }
+    (HERE / "rng.json").write_text(json.dumps(out, indent=1))
+
+
+def make_setup():
+    d = {}
+    for n in (2, 3, 10, 64, 100, 256):
+        d[f"sigma_{n}"] = np.array(op.solve_sigma(n))
+        p, _ = op.build_phi_op(n)
+        d[f"phi_{n}"] = np.stack([p.a, np.append(p.b, 0), np.append(p.c, 0), p.grid])
+    for dd, n in ((2, 2), (2, 64), (3, 3), (3, 100), (2, 128)):
+        r = op.build_rho(dd, n, 1.0)
+        d[f"rho{dd}_{n}"] = np.stack([r.a, np.append(r.b, 0), np.append(r.c, 0), r.grid])
+    for n, lam in ((128, -1.95), (16, -1.0), (8, 0.0)):
+        r = op.build_lambda(n, 1.0, lam)
+        d[f"lambda_{n}_{lam}"] = np.stack([r.a, np.append(r.b, 0), np.append(r.c, 0), r.grid])
+    for n in (3, 4, 5, 8, 16):
+        fac = op.eig_theta(op.build_theta(n))
+        d[f"eigtheta_{n}_Q"] = fac.Q
+        d[f"eigtheta_{n}_lam"] = fac.lambdas
+    for name, o in (("rho2_64", op.build_rho(2, 64, 1.0)), ("phi_100", op.build_phi_op(100)[0]),
+                    ("lambda_128", op.build_lambda(128, 1.0, -1.95)), ("z_16", op.build_z(16, 2.0))):
+        fac = op.eig_tridiag(o)
+        d[f"eig_{name}_lam"] = fac.lambdas
+        d[f"eig_{name}_Vabs"] = np.abs(fac.V)  # column signs are LAPACK's choice
+        d[f"eig_{name}_xi"] = fac.xi
+        d[f"phi1m_{name}"] = phi1_matrix(0.0123, fac)
+    x = np.concatenate([-np.logspace(-9, 2, 40), np.logspace(-9, 1.5, 40), [0.0, 1e-5, -1e-5, 9.99e-6]])
+    d["phi1_x"] = x
+    d["phi1_y"] = phi1(x)
+    rs = np.random.RandomState(5)
+    f1, f2, f3 = -rs.rand(5), -rs.rand(6) * 30, rs.rand(4)
+    d["outer_f"] = np.concatenate([f1, f2, f3])
+    d["outer2"] = phi1_outer(0.37, [f1, f2]).field
+    d["outer3"] = phi1_outer(0.37, [f1, f2, f3]).field
+    np.savez_compressed(HERE / "setup.npz", **d)
+
+
+def _bases():
+    return {
+        "disk_4x4": ComponentOps(Geometry.DISK, 0.7, rho=op.build_rho(2, 4, 1.0), theta=op.build_theta(4)),
+        "sphere_4x4": ComponentOps(Geometry.SPHERE, 0.9, theta=op.build_theta(4), phi=op.build_phi_op(4)[0]),
+        "ball_3x4x4": ComponentOps(Geometry.BALL, 1.1, rho=op.build_rho(3, 3, 1.0), theta=op.build_theta(4),
+                                   phi=op.build_phi_op(4)[0]),
+        "cylinder_3x4x4": ComponentOps(Geometry.CYLINDER, 0.8, rho=op.build_rho(2, 3, 1.0),
+                                       theta=op.build_theta(4), z=op.build_z(4, 1.0)),
+        "disk_20x36": ComponentOps(Geometry.DISK, 1.3, rho=op.build_rho(2, 20, 1.0), theta=op.build_theta(36)),
+        "adisk_33x64": ComponentOps(Geometry.DISK, 10.0, rho=op.build_lambda(33, 1.0, -1.95),
+                                    theta=op.build_theta(64),
+                                    rho_weights=op.DiagonalWeights(op.build_lambda(33, 1.0, -1.95).grid ** (-2.0 + 1.95))),
+        "sphere_40x34": ComponentOps(Geometry.SPHERE, 0.08, theta=op.build_theta(40), phi=op.build_phi_op(34)[0]),
+        "ball_12x10x18": ComponentOps(Geometry.BALL, 0.516, rho=op.build_rho(3, 12, 1.0),
+                                      theta=op.build_theta(10), phi=op.build_phi_op(18)[0]),
+        "cylinder_9x20x24": ComponentOps(Geometry.CYLINDER, 2e-2, rho=op.build_rho(2, 9, 1.0),
+                                         theta=op.build_theta(20), z=z_neumann(24, 2.0)),
+        "cylinderD_6x8x10": ComponentOps(Geometry.CYLINDER, 0.3, rho=op.build_rho(2, 6, 1.0),
+                                         theta=op.build_theta(8), z=op.build_z(10, 1.5)),
+    }
+
+
+def make_steps():
+    d = {}
+    rs = np.random.RandomState(22)
+    for name, base in _bases().items():
+        for tau in (0.037, 0.0):
+            ops = prepare(base, tau)
+            W = rs.randn(*base.shape)
+            G = rs.randn(*base.shape)
+            key = f"{name}_tau{tau}"
+            d[key + "_W"] = W
+            d[key + "_G"] = G
+            d[key + "_MW"] = apply_diffusion(ops, W)
+            d[key + "_out"] = step_split(ops, W, G)
+    np.savez_compressed(HERE / "steps.npz", **d)
+
+
+def make_runs():
+    d = {}
+    for k in (1, 2, 3, 4):
+        sysm = ref_config(k, SMALL[k])
+        m = 20
+        t = STEPS[k][1] / STEPS[k][0] * m
+        res = run_simulation(sysm, m, t)
+        for c in sysm.components:
+            d[f"c{k}_{c.name}_init"] = c.initial
+            d[f"c{k}_{c.name}_final"] = physical(sysm, res.fields)[c.name]
+        d[f"c{k}_m"] = np.array(m)
+        d[f"c{k}_t"] = np.array(t)
+    for i in (0, 7, 511):
+        sysm = ref_member(i, SMALL[5])
+        m = 20
+        res = run_simulation(sysm, m, 0.02)
+        for c in sysm.components:
+            d[f"c5m{i}_{c.name}_init"] = c.initial
+            d[f"c5m{i}_{c.name}_final"] = physical(sysm, res.fields)[c.name]
+    np.savez_compressed(HERE / "runs.npz", **d)
+
+
+def _sample_idx(n):
+    return np.unique(np.linspace(0, n - 1, SAMPLES).astype(np.int64))
+
+
+def _record(d, key, sysm, states):
+    phys = physical(sysm, states)
+    for c in sysm.components:
+        f = phys[c.name].ravel()
+        idx = _sample_idx(f.size)
+        d[f"{key}_{c.name}_idx"] = idx
+        d[f"{key}_{c.name}_val"] = f[idx]
+        d[f"{key}_{c.name}_maxabs"] = np.array(np.max(np.abs(f)))
+        d[f"{key}_{c.name}_sum"] = np.array(np.sum(f))
+
+
+def make_full():
+    d = {}
+    for k in (1, 2, 3, 4):
+        t0 = time.time()
+        sysm = ref_config(k, FULL[k])
+        m, ts = STEPS[k]
+        tau = ts / m
+        for c in sysm.components:
+            d[f"f{k}_{c.name}_init_sum"] = np.array(np.sum(c.initial))
+            d[f"f{k}_{c.name}_init_sample"] = c.initial.ravel()[_sample_idx(c.initial.size)]
+        r1 = run_simulation(sysm, 1, tau)
+        _record(d, f"f{k}_s1", sysm, r1.fields)
+        r100 = run_simulation(sysm, 100, 100 * tau)
+        _record(d, f"f{k}_s100", sysm, r100.fields)
+        print(f"config {k}: {time.time() - t0:.1f}s", flush=True)
+    for i in (0, 255, 511):
+        sysm = ref_member(i, FULL[5])
+        for c in sysm.components:
+            d[f"f5m{i}_{c.name}_init_sum"] = np.array(np.sum(c.initial))
+            d[f"f5m{i}_{c.name}_init_sample"] = c.initial.ravel()[_sample_idx(c.initial.size)]
+        r1 = run_simulation(sysm, 1, 1e-3)
+        _record(d, f"f5m{i}_s1", sysm, r1.fields)
+        r100 = run_simulation(sysm, 100, 0.1)
+        _record(d, f"f5m{i}_s100", sysm, r100.fields)
+    np.savez_compressed(HERE / "full.npz", **d)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["rng", "setup", "steps", "runs", "full"]
+    for w in which:
+        t0 = time.time()
+        globals()[f"make_{w}"]()
+        print(f"{w}: {time.time() - t0:.1f}s", flush=True)

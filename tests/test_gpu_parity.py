@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path (through libcurvigpu's C ABI) against the
+reference's golden fixtures and the CPU oracle on identical seeded inputs.
+
+Tolerance (north_star): relative inf-norm on physical fields <= 1e-10 after
+1 step and <= 1e-8 after 100 steps.  Single operations (diffusion action,
+one split step on random data) are held to 1e-12.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import configs as ocfg
+from oracle import curvi_oracle as orc
+from paper_2604_11558_b200 import configs as pcfg
+from paper_2604_11558_b200.integrators import (
+    INT32_MAX,
+    DivergenceError,
+    SplitPlan,
+    apply_diffusion,
+    prepare,
+    run_simulation,
+    step_split,
+)
+
+from ._cases import CASES, engine_base
+from .conftest import rel_inf
+
+pytestmark = pytest.mark.gpu
+
+SMALL = {1: (16, 32), 2: (24, 16), 3: (8, 16, 16), 4: (10, 12, 10), 5: (16, 32)}
+STEP1_TOL = 1e-10
+STEP100_TOL = 1e-8
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_apply_diffusion_matches_reference(golden, name):
+    base = engine_base(name)
+    for tau in (0.037, 0.0):
+        key = f"{name}_tau{tau}"
+        out = apply_diffusion(prepare(base, tau), golden.steps[key + "_W"])
+        assert rel_inf(out, golden.steps[key + "_MW"]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_step_split_matches_reference(golden, name):
+    base = engine_base(name)
+    for tau in (0.037, 0.0):
+        key = f"{name}_tau{tau}"
+        W, G = golden.steps[key + "_W"], golden.steps[key + "_G"]
+        out = step_split(prepare(base, tau), W, G)
+        if tau == 0.0:
+            assert np.array_equal(out, W)  # reference tests/test_integrators.py:116-123
+        assert rel_inf(out, golden.steps[key + "_out"]) <= 1e-12
+
+
+def test_step_split_torch_in_torch_out(golden):
+    import torch
+
+    key = "disk_20x36_tau0.037"
+    W = torch.from_numpy(golden.steps[key + "_W"]).cuda()
+    G = torch.from_numpy(golden.steps[key + "_G"]).cuda()
+    out = step_split(prepare(engine_base("disk_20x36"), 0.037), W, G)
+    assert isinstance(out, torch.Tensor) and out.is_cuda
+    assert rel_inf(out.cpu().numpy(), golden.steps[key + "_out"]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["disk_20x36", "sphere_40x34", "ball_12x10x18", "cylinder_9x20x24"])
+def test_constants_are_fixed_points(name):
+    base = engine_base(name)
+    ops = prepare(base, 0.05)
+    W = np.full(base.shape, 3.7)
+    out = step_split(ops, W, np.zeros(base.shape))
+    if name.startswith("cylinder_9"):  # Neumann-Neumann z: constants are fixed too
+        assert np.max(np.abs(out - W)) <= 1e-10
+    else:
+        assert np.max(np.abs(out - W)) <= 1e-10
+
+
+def test_zero_field_is_fixed_bitwise_cylinder_dirichlet():
+    base = engine_base("cylinderD_6x8x10")
+    zero = np.zeros(base.shape)
+    assert np.array_equal(step_split(prepare(base, 0.05), zero, zero), zero)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_small_config_runs_match_reference(golden, k):
+    r = golden.runs
+    sysm = pcfg.BUILDERS[k](SMALL[k])
+    res = run_simulation(sysm, int(r[f"c{k}_m"]), float(r[f"c{k}_t"]))
+    for c in sysm.components:
+        assert rel_inf(res.fields[c.name] + c.lift, r[f"c{k}_{c.name}_final"]) <= STEP1_TOL
+
+
+def test_small_ensemble_members_match_reference(golden):
+    from paper_2604_11558_b200.ensemble import run_ensemble
+
+    members = [pcfg.config5_member(i, SMALL[5]) for i in (0, 7, 511)]
+    res = run_ensemble(members, 20, 0.02)
+    for j, i in enumerate((0, 7, 511)):
+        for ci, name in enumerate(("u", "v")):
+            assert rel_inf(res.fields[j, ci], golden.runs[f"c5m{i}_{name}_final"]) <= STEP1_TOL
+    assert (res.first_bad == INT32_MAX).all()
+
+
+def _check_samples(full, key, fields, tol):
+    for name, f in fields.items():
+        flat = np.asarray(f).ravel()
+        idx = full[f"{key}_{name}_idx"]
+        err = np.max(np.abs(flat[idx] - full[f"{key}_{name}_val"])) / full[f"{key}_{name}_maxabs"]
+        assert err <= tol, (key, name, err)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_full_config_matches_reference_at_steps_1_and_100(golden, k):
+    full = golden.full
+    sysm = pcfg.BUILDERS[k]()
+    m, ts = pcfg.STEPS[k]
+    tau = ts / m
+    lifts = {c.name: c.lift for c in sysm.components}
+    r1 = run_simulation(sysm, 1, tau)
+    _check_samples(full, f"f{k}_s1", {n: v + lifts[n] for n, v in r1.fields.items()}, STEP1_TOL)
+    r100 = run_simulation(sysm, 100, 100 * tau)
+    _check_samples(full, f"f{k}_s100", {n: v + lifts[n] for n, v in r100.fields.items()}, STEP100_TOL)
+    # whole field against the oracle on the same inputs after 1 step
+    osys = ocfg.BUILDERS[k](initial=[c.initial for c in sysm.components])
+    ref = orc.physical(osys, orc.integrate(osys, 1, tau))
+    for c in sysm.components:
+        assert rel_inf(r1.fields[c.name] + c.lift, ref[c.name]) <= STEP1_TOL
+
+
+def _ensemble_plan(inputs, tau):
+    from paper_2604_11558_b200.ensemble import ensemble_plan
+
+    params = np.stack([[g, 0.1, 0.9] for g in inputs.gammas])
+    return ensemble_plan(inputs.template, "schnakenberg", params, tau)
+
+
+def test_full_ensemble_matches_reference_and_oracle(golden):
+    import torch
+
+    full = golden.full
+    ens = pcfg.config5_inputs(0, 512)
+    plan = _ensemble_plan(ens, 1e-3)
+    state = torch.from_numpy(ens.states).cuda()
+    bad = torch.full((512, 2), INT32_MAX, dtype=torch.int32, device="cuda")
+    plan.run(state, 0, 1, bad)
+    s1 = state.cpu().numpy()
+    lifts = np.array([1.0, 0.9 / 1.0**2])
+    for i in (0, 255, 511):
+        _check_samples(full, f"f5m{i}_s1", {"u": s1[i, 0] + lifts[0], "v": s1[i, 1] + lifts[1]}, STEP1_TOL)
+    # every member against the oracle after one step
+    worst = 0.0
+    for i in range(0, 512, 7):
+        osys = ocfg.config5_member(i, initial=[ens.states[i, 0], ens.states[i, 1]])
+        ref = orc.physical(osys, orc.integrate(osys, 1, 1e-3))
+        worst = max(worst, rel_inf(s1[i, 0] + lifts[0], ref["u"]), rel_inf(s1[i, 1] + lifts[1], ref["v"]))
+    assert worst <= STEP1_TOL
+    plan.run(state, 1, 99, bad)
+    s100 = state.cpu().numpy()
+    for i in (0, 255, 511):
+        _check_samples(full, f"f5m{i}_s100", {"u": s100[i, 0] + lifts[0], "v": s100[i, 1] + lifts[1]},
+                       STEP100_TOL)
+    assert (bad.cpu().numpy() == INT32_MAX).all()
+
+
+@pytest.mark.slow
+def test_full_horizon_config1_and_ensemble_members_vs_oracle():
+    import torch
+
+    sysm = pcfg.config1()
+    res = run_simulation(sysm, 1000, 1.0)
+    osys = ocfg.config1(initial=[c.initial for c in sysm.components])
+    ref = orc.integrate(osys, 1000, 1.0)
+    for c in sysm.components:
+        assert rel_inf(res.fields[c.name], ref[c.name]) <= STEP100_TOL
+    ens = pcfg.config5_inputs(509, 3)
+    plan = _ensemble_plan(ens, 1e-3)
+    state = torch.from_numpy(ens.states).cuda()
+    bad = torch.full((3, 2), INT32_MAX, dtype=torch.int32, device="cuda")
+    plan.run(state, 0, 1000, bad)
+    out = state.cpu().numpy()
+    osys = ocfg.config5_member(511, initial=[ens.states[2, 0], ens.states[2, 1]])
+    ref = orc.physical(osys, orc.integrate(osys, 1000, 1.0))
+    assert rel_inf(out[2, 0] + 1.0, ref["u"]) <= STEP100_TOL
+    assert rel_inf(out[2, 1] + 0.9, ref["v"]) <= STEP100_TOL
+
+
+def test_divergence_names_the_oracle_step():
+    from paper_2604_11558_b200.models import Kinetics
+
+    sysm = pcfg.config1(SMALL[1])
+    wild = type(sysm)(spec=None, components=sysm.components,
+                      kinetics=Kinetics("schnakenberg", {"gamma": 3.0e4, "a": 0.1, "b": 0.9}), equilibrium={})
+    osys = ocfg.config1(SMALL[1], initial=[c.initial for c in sysm.components])
+    osys.params["gamma"] = 3.0e4
+    with pytest.raises(orc.OracleDivergence) as ref_err:
+        orc.integrate(osys, 200, 0.2)
+    with pytest.raises(DivergenceError) as err:
+        run_simulation(wild, 200, 0.2, record_every=7)
+    assert err.value.step == ref_err.value.step
+
+
+def test_reruns_are_bitwise_identical():
+    sysm = pcfg.config4((10, 12, 10))
+    a = run_simulation(sysm, 37, 0.37)
+    b = run_simulation(sysm, 37, 0.37)
+    for n in a.fields:
+        assert np.array_equal(a.fields[n], b.fields[n])
+
+
+def test_graph_chunks_equal_eager_steps():
+    import torch
+
+    sysm = pcfg.config1(SMALL[1])
+    geos = [prepare(c.ops, 1e-3) for c in sysm.components]
+    plan = SplitPlan(geos, 1, "schnakenberg", sysm.kinetics.param_vector()[None, :])
+    init = torch.from_numpy(np.stack([c.initial for c in sysm.components])[None]).cuda()
+    bad = torch.full((1, 2), INT32_MAX, dtype=torch.int32, device="cuda")
+    a = init.clone()
+    plan.run(a, 0, 35, bad)  # two 16-step graph replays + 3 eager steps
+    b = init.clone()
+    for s in range(35):
+        plan.run(b, s, 1, bad)
+    assert torch.equal(a, b)
+
+
+def test_sampling_schedule_and_hook():
+    sysm = pcfg.config1(SMALL[1])
+    seen = []
+    res = run_simulation(sysm, 10, 0.01, record_every=4,
+                         diagnostics=lambda st: {n: float(np.mean(v)) for n, v in st.items()},
+                         sample_hook=lambda step, t, st: seen.append(step))
+    assert seen == [0, 4, 8, 10]
+    assert len(res.times) == 4 and len(res.series["u"]) == 4
+
+
+@pytest.mark.parametrize("kind,params", [
+    ("schnakenberg", {"gamma": 100.0, "a": 0.1, "b": 0.9}),
+    ("brusselator", {"A": 4.5, "B": 6.96}),
+    ("gray_scott", {"F": 0.04, "k": 0.06}),
+    ("bvam_eta", {"eta": 0.45, "a": 1.112, "b": -1.01, "h": -1.0, "C": 0.02}),
+    ("bvam", {"alpha1": 0.899, "alpha2": 0.2, "alpha3": 0.2, "beta1": -0.91, "beta2": -0.899}),
+])
+def test_kinetics_kernel_bitwise_vs_oracle(kind, params):
+    import torch
+
+    from paper_2604_11558_b200.models import Kinetics
+
+    base = engine_base("disk_20x36")
+    kin = Kinetics(kind, params)
+    geos = [prepare(base, 0.01), prepare(base, 0.01)]
+    plan = SplitPlan(geos, 2, kind, np.stack([kin.param_vector()] * 2), lifts=[0.25, -0.5])
+    rs = np.random.RandomState(3)
+    W = rs.randn(2, 2, *base.shape)
+    G = torch.empty((2, 2) + base.shape, dtype=torch.float64, device="cuda")
+    plan.kinetics_into(torch.from_numpy(W).cuda(), G)
+    got = G.cpu().numpy()
+    for b in range(2):
+        ref = orc.kinetics(kind, params, {"u": W[b, 0], "v": W[b, 1]}, ["u", "v"], [0.25, -0.5])
+        assert np.array_equal(got[b, 0], ref["u"]), kind
+        assert np.array_equal(got[b, 1], ref["v"]), kind
