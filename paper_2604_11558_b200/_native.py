@@ -72,6 +72,9 @@ EXPORTS = (
     "cg_rng_next",
     "cg_rng_uniform",
     "cg_rng_normal",
+    "cg_plan_stage_count",
+    "cg_plan_stage_info",
+    "cg_run_stage",
 )
 
 
@@ -116,6 +119,13 @@ def lib():
     L.cg_rng_uniform.restype = None
     L.cg_rng_normal.argtypes = [u64p, ctypes.c_longlong, ctypes.c_double, dp]
     L.cg_rng_normal.restype = None
+    L.cg_plan_stage_count.argtypes = [vp]
+    L.cg_plan_stage_count.restype = ctypes.c_int
+    L.cg_plan_stage_info.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong),
+                                     ctypes.POINTER(ctypes.c_longlong)]
+    L.cg_plan_stage_info.restype = ctypes.c_int
+    L.cg_run_stage.argtypes = [vp, ctypes.c_int, vp, vp, vp, vp]
+    L.cg_run_stage.restype = ctypes.c_int
     _lib = L
     return L
 

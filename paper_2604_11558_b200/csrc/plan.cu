@@ -290,9 +290,8 @@ int add_stage(cg_plan* p, int var, int epi, int M, int N, int K, int nslab, int 
 
 double* buf_ptr(cg_plan* p, int id, double* out) { return id == BUF_X ? p->X : id == BUF_Y ? p->Y : out; }
 
-// Launch one full step: Win (+G) -> F -> stage chain -> Wout.
-int launch_step(cg_plan* p, const double* Win, double* Wout, const double* Gext, bool fused_kin, int* first_bad,
-                bool count_step, cudaStream_t s) {
+int launch_fstage(cg_plan* p, const double* Win, const double* Gext, bool fused_kin, bool count_step,
+                  cudaStream_t s) {
   StencilParams sp{};
   sp.geometry = p->geom;
   sp.n1 = p->n1;
@@ -317,10 +316,12 @@ int launch_step(cg_plan* p, const double* Win, double* Wout, const double* Gext,
   sp.with_diffusion = 1;
   sp.with_reaction = 1;
   sp.step = count_step ? p->step_dev : nullptr;
-  int rc = launch_fbuild(p->geom, fused_kin ? p->kin : KIN_EXTERNAL, sp, s);
-  if (rc) return rc;
+  return launch_fbuild(p->geom, fused_kin ? p->kin : KIN_EXTERNAL, sp, s);
+}
 
-  for (const Stage& st : p->stages) {
+int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, int* first_bad, cudaStream_t s) {
+  int rc;
+  {
     const double* src = buf_ptr(p, st.src, Wout);
     double* dst = buf_ptr(p, st.dst, Wout);
     CUtensorMap smap;
@@ -370,6 +371,16 @@ int launch_step(cg_plan* p, const double* Win, double* Wout, const double* Gext,
       rc = launch_gemm(st.var, st.epi, st.cfg, st.opmap, smap, gp, s);
     if (rc) return rc;
   }
+  return CG_OK;
+}
+
+// Launch one full step: Win (+G) -> F -> stage chain -> Wout.
+int launch_step(cg_plan* p, const double* Win, double* Wout, const double* Gext, bool fused_kin, int* first_bad,
+                bool count_step, cudaStream_t s) {
+  int rc = launch_fstage(p, Win, Gext, fused_kin, count_step, s);
+  if (rc) return rc;
+  for (const Stage& st : p->stages)
+    if ((rc = launch_stage(p, st, Win, Wout, first_bad, s))) return rc;
   return CG_OK;
 }
 
@@ -613,6 +624,30 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
   if (e != cudaSuccess) return bail(fail(CG_ECUDA, cudaGetErrorString(e)));
   *out = p;
   return CG_OK;
+}
+
+int cg_plan_stage_count(const cg_plan* p) { return p ? (int)p->stages.size() : 0; }
+
+int cg_plan_stage_info(const cg_plan* p, int stage, long long* flops, long long* bytes) {
+  if (!p || stage < -1 || stage >= (int)p->stages.size()) return fail(CG_EINVAL, "bad stage index");
+  if (stage < 0) {
+    if (flops) *flops = 0;
+    if (bytes) *bytes = 2LL * p->elems * (long long)sizeof(double);  // read W once, write F once
+    return CG_OK;
+  }
+  const Stage& st = p->stages[stage];
+  const long long items = (long long)p->B * p->C * st.nslab;
+  if (flops) *flops = 2LL * st.M * st.N * st.K * items;
+  if (bytes) *bytes = (st.epi == EPI_AXPY ? 3LL : 2LL) * p->elems * (long long)sizeof(double);
+  return CG_OK;
+}
+
+int cg_run_stage(cg_plan* p, int stage, const double* W, double* W_out, int* first_bad, void* stream) {
+  if (!p || !W || !W_out) return fail(CG_EINVAL, "null argument");
+  if (stage < -1 || stage >= (int)p->stages.size()) return fail(CG_EINVAL, "bad stage index");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (stage < 0) return launch_fstage(p, W, nullptr, p->kin != CG_KIN_EXTERNAL, false, s);
+  return launch_stage(p, p->stages[stage], W, W_out, first_bad ? first_bad : p->scratch_bad, s);
 }
 
 int cg_apply_diffusion(cg_plan* p, const double* W, double* out, void* stream) {

@@ -344,6 +344,24 @@ class SplitPlan:
         _native.check(self._lib.cg_step(self._h, W.data_ptr(), G.data_ptr(), out.data_ptr(), self._stream()),
                       "cg_step")
 
+    # -- measurement access (bench.py) ---------------------------------------
+    def stage_count(self) -> int:
+        return int(self._lib.cg_plan_stage_count(self._h))
+
+    def stage_info(self, stage: int) -> tuple[int, int]:
+        """(algorithmic flops, algorithmic HBM bytes) of one launch of a
+        stage; stage -1 is the F-build kernel."""
+        fl, by = ctypes.c_longlong(), ctypes.c_longlong()
+        _native.check(self._lib.cg_plan_stage_info(self._h, int(stage), ctypes.byref(fl), ctypes.byref(by)),
+                      "cg_plan_stage_info")
+        return int(fl.value), int(by.value)
+
+    def run_stage(self, stage: int, W, out):
+        self._check_state(W, "W")
+        self._check_state(out, "out")
+        _native.check(self._lib.cg_run_stage(self._h, int(stage), W.data_ptr(), out.data_ptr(), None,
+                                             self._stream()), "cg_run_stage")
+
     def run(self, state, step0: int, nsteps: int, first_bad):
         """Advance ``state`` in place; ``first_bad`` is an int32 CUDA tensor
         of shape (batch, ncomp) receiving the first diverged step per field."""
