@@ -216,30 +216,56 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
   bool bad = false;
   int step_now = 0;
   if (EPI == EPI_AXPY) step_now = *p.step;
+  // Gather the epilogue operands (W pair or two phi1 values per accumulator
+  // pair) for a group of EC fragment rows with all loads in flight at once,
+  // then combine and store: load latency is paid once per group instead of
+  // once per fragment.  EC < MT bounds the registers at 2+ CTAs per SM.
+  constexpr int EC = (MINB >= 2 && MT > 2) ? MT / 2 : MT;
 #pragma unroll
-  for (int i = 0; i < MT; ++i) {
-    const int m = m0 + wm0 + i * 8 + row_in8;
-    if (m >= p.M) continue;
-    const double* phirow = nullptr;
-    if (EPI == EPI_PHI)
-      phirow = p.phi + c * p.phi_c + s * p.phi_s + (long long)(m / p.phi_rdiv) * p.phi_m;
+  for (int i0 = 0; i0 < MT; i0 += EC) {
+    double2 opnd[EC][NT];
+    if (EPI != EPI_STORE) {
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      const int n = n0 + wn0 + j * 8 + col_in8;
-      if (n >= p.N) continue;
-      const long long idx = base + (long long)m * p.ldc + n;
-      double v0 = acc[i][j][0], v1 = acc[i][j][1];
-      if (EPI == EPI_PHI) {
-        v0 *= __ldg(phirow + (long long)n * p.phi_n);
-        v1 *= __ldg(phirow + (long long)(n + 1) * p.phi_n);
-      } else if (EPI == EPI_AXPY) {
-        const double2 w2 = __ldg(reinterpret_cast<const double2*>(p.w + idx));
-        // W + tau*T rounded as the reference rounds it (no FMA contraction)
-        v0 = __dadd_rn(w2.x, __dmul_rn(p.tau, v0));
-        v1 = __dadd_rn(w2.y, __dmul_rn(p.tau, v1));
-        bad |= !(fabs(v0) <= p.limit) || !(fabs(v1) <= p.limit);
+      for (int ii = 0; ii < EC; ++ii) {
+        int m = m0 + wm0 + (i0 + ii) * 8 + row_in8;
+        if (m >= p.M) m = 0;
+        const double* phirow = nullptr;
+        if (EPI == EPI_PHI) phirow = p.phi + c * p.phi_c + s * p.phi_s + (long long)(m / p.phi_rdiv) * p.phi_m;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          int n = n0 + wn0 + j * 8 + col_in8;
+          if (n >= p.N) n = 0;
+          if (EPI == EPI_PHI) {
+            opnd[ii][j].x = __ldg(phirow + (long long)n * p.phi_n);
+            opnd[ii][j].y = __ldg(phirow + (long long)(n + 1) * p.phi_n);
+          } else {
+            opnd[ii][j] = __ldg(reinterpret_cast<const double2*>(p.w + base + (long long)m * p.ldc + n));
+          }
+        }
       }
-      *reinterpret_cast<double2*>(p.out + idx) = make_double2(v0, v1);
+    }
+#pragma unroll
+    for (int ii = 0; ii < EC; ++ii) {
+      const int i = i0 + ii;
+      const int m = m0 + wm0 + i * 8 + row_in8;
+      if (m >= p.M) continue;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int n = n0 + wn0 + j * 8 + col_in8;
+        if (n >= p.N) continue;
+        const long long idx = base + (long long)m * p.ldc + n;
+        double v0 = acc[i][j][0], v1 = acc[i][j][1];
+        if (EPI == EPI_PHI) {
+          v0 *= opnd[ii][j].x;
+          v1 *= opnd[ii][j].y;
+        } else if (EPI == EPI_AXPY) {
+          // W + tau*T rounded as the reference rounds it (no FMA contraction)
+          v0 = __dadd_rn(opnd[ii][j].x, __dmul_rn(p.tau, v0));
+          v1 = __dadd_rn(opnd[ii][j].y, __dmul_rn(p.tau, v1));
+          bad |= !(fabs(v0) <= p.limit) || !(fabs(v1) <= p.limit);
+        }
+        *reinterpret_cast<double2*>(p.out + idx) = make_double2(v0, v1);
+      }
     }
   }
   if (EPI == EPI_AXPY) {

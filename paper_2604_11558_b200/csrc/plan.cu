@@ -13,6 +13,7 @@
 
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -83,21 +84,25 @@ int make_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
 struct TileCfg {
   int BM, BN;
 };
-constexpr int kNumCfg = 3;
-constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}};
+constexpr int kNumCfg = 7;
+constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {64, 128}, {128, 128}, {64, 64}};
 
 // BM, BN, warp tile, stages; 32x32 warp tiles keep the accumulators +
 // fragments under ~160 registers without spills.
-#define CFG0 128, 64, 32, 32, 4
-#define CFG1 64, 128, 32, 32, 4
-#define CFG2 64, 64, 32, 32, 4
+// (BM, BN, warp tile WM x WN, stages, min CTAs per SM)
+#define CFG0 128, 64, 32, 32, 4, 1
+#define CFG1 64, 128, 32, 32, 4, 1
+#define CFG2 64, 64, 32, 32, 4, 2
+#define CFG3 128, 64, 32, 32, 4, 2
+#define CFG4 64, 128, 32, 32, 4, 2
+#define CFG5 128, 128, 32, 32, 3, 1
+#define CFG6 64, 64, 32, 32, 6, 3
 
 // configure_only: set the dynamic shared memory opt-in (done at plan
 // creation, never inside a stream capture).
-template <int VAR, int BM, int BN, int WM, int WN, int ST, int EPI>
+template <int VAR, int BM, int BN, int WM, int WN, int ST, int MINB, int EPI>
 int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams& p, cudaStream_t stream,
                   bool configure_only) {
-  constexpr int MINB = ((BM / WM) * (BN / WN) <= 4) ? 2 : 1;
   auto kern = gemm_f64_kernel<VAR, BM, BN, WM, WN, ST, EPI, MINB>;
   constexpr int smem = gemm_smem_bytes<BM, BN, ST>();
   if (configure_only) {
@@ -119,7 +124,11 @@ int launch_gemm_cfg(int cfg, const CUtensorMap& ma, const CUtensorMap& mb, const
   switch (cfg) {
     case 0: return launch_gemm_t<VAR, CFG0, EPI>(ma, mb, p, stream, conf);
     case 1: return launch_gemm_t<VAR, CFG1, EPI>(ma, mb, p, stream, conf);
-    default: return launch_gemm_t<VAR, CFG2, EPI>(ma, mb, p, stream, conf);
+    case 2: return launch_gemm_t<VAR, CFG2, EPI>(ma, mb, p, stream, conf);
+    case 3: return launch_gemm_t<VAR, CFG3, EPI>(ma, mb, p, stream, conf);
+    case 4: return launch_gemm_t<VAR, CFG4, EPI>(ma, mb, p, stream, conf);
+    case 5: return launch_gemm_t<VAR, CFG5, EPI>(ma, mb, p, stream, conf);
+    default: return launch_gemm_t<VAR, CFG6, EPI>(ma, mb, p, stream, conf);
   }
 }
 
@@ -139,12 +148,14 @@ __global__ void set_step_kernel(int* step, int value) { *step = value; }
 
 template <int GEOM, int KIN>
 int launch_fbuild_t(const StencilParams& p, cudaStream_t s) {
-  const long long total = p.npts * p.batch;
-  long long blocks = (total + 255) / 256;
-  const long long cap = 148LL * 16;
-  if (blocks > cap) blocks = cap;
-  if (blocks < 1) blocks = 1;
-  fbuild_kernel<GEOM, KIN><<<(unsigned)blocks, 256, 0, s>>>(p);
+  if (p.batch > 65535) return fail(CG_EUNSUPPORTED, "batch > 65535 runs per plan");
+  const bool d3 = GEOM >= 2;
+  const int nl = d3 ? p.n3 : p.n2;
+  if (nl > 512) return fail(CG_EUNSUPPORTED, "contiguous axis longer than 512");
+  constexpr int RB = 8;
+  const dim3 grid((unsigned)((p.n1 + RB - 1) / RB), d3 ? (unsigned)p.n2 : 1u, (unsigned)p.batch);
+  const unsigned threads = (unsigned)((nl + 31) / 32 * 32);
+  fbuild_rows_kernel<GEOM, KIN, RB><<<grid, threads, 0, s>>>(p);
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
 }
@@ -255,14 +266,28 @@ int upload_operator(cg_plan* p, int var, int n, Get get, double** out, CUtensorM
   return make_map(map, *out, 3, dims, strides, box);
 }
 
-int pick_cfg(int var, long long nbatch, int M, int N) {
-  // largest tile that still gives >= 2 waves of 148 SMs (or the smallest tile)
-  for (int c = 0; c < kNumCfg; ++c) {
-    const long long ctas = nbatch * ((M + kCfgs[c].BM - 1) / kCfgs[c].BM) * ((N + kCfgs[c].BN - 1) / kCfgs[c].BN);
-    if (ctas >= 2 * 148) return c;
+int pick_cfg(int var, long long nbatch, int M, int N, int stage_index) {
+  // measurement override: CURVIGPU_TILE_CFG=<cfg> or "<s0>,<s1>,..." per stage
+  if (const char* env = getenv("CURVIGPU_TILE_CFG")) {
+    int vals[16], nv = 0;
+    for (const char* q = env; *q && nv < 16;) {
+      vals[nv++] = atoi(q);
+      while (*q && *q != ',') ++q;
+      if (*q == ',') ++q;
+    }
+    const int v = nv == 1 ? vals[0] : (stage_index < nv ? vals[stage_index] : -1);
+    if (v >= 0 && v < kNumCfg) return v;
   }
-  (void)var;
-  return kNumCfg - 1;
+  // Measured on B200 (tools/sweep_tiles.py, profiles/r01_tile_sweep.txt):
+  // NN stages are best with 64x64 tiles, 2 CTAs/SM; TN stages with 64x128
+  // tiles at 2 CTAs/SM when N is a multiple of 128 and there are >= 2 waves,
+  // else 64x64 with a 6-deep ring at 3 CTAs/SM.
+  auto ctas = [&](int c) {
+    return nbatch * ((M + kCfgs[c].BM - 1) / kCfgs[c].BM) * ((N + kCfgs[c].BN - 1) / kCfgs[c].BN);
+  };
+  if (var == VAR_NN) return 2;
+  if (N % 128 == 0 && ctas(4) >= 2 * 148) return 4;
+  return 6;
 }
 
 // Build one GEMM stage: operator L (n x n) via `get`, shapes, epilogue.
@@ -279,7 +304,7 @@ int add_stage(cg_plan* p, int var, int epi, int M, int N, int K, int nslab, int 
   st.dst = dst;
   st.phi_rdiv = 1;
   const long long nbatch = (long long)p->B * p->C * nslab;
-  st.cfg = pick_cfg(var, nbatch, M, N);
+  st.cfg = pick_cfg(var, nbatch, M, N, (int)p->stages.size());
   double* op = nullptr;
   const int box_rows = (var == VAR_TN) ? kCfgs[st.cfg].BN : 16;
   int rc = upload_operator(p, var, n_op, get, &op, &st.opmap, box_rows);

@@ -136,26 +136,181 @@ __device__ __forceinline__ void reaction(const double* k, double u, double v, do
 #undef SUB
 }
 
+// ---------------------------------------------------------------------------
+// Register-blocked F-build.  Lanes run along the contiguous axis (coalesced
+// loads/stores; in-row neighbours come from warp shuffles), each thread walks
+// RB consecutive points of the first axis with a 3-value sliding window, so
+// every W value is read from memory about once (the naive one-thread-per-
+// point kernel re-read 5-7 neighbours per point and was L1-bound).
+//   grid = (ceil(n1 / RB), 3-D ? n2 : 1, batch), block = round32(n_last)
+// ---------------------------------------------------------------------------
+
+struct Win {
+  double m, c, p;
+};
+
+// three-point tridiagonal row: c_{i-1} x_{i-1} + a_i x_i + b_i x_{i+1}
+__device__ __forceinline__ double tri3(const double* bands, int n, int i, double xm, double x0, double xp) {
+  double y = bands[i] * x0;
+  if (i > 0) y += bands[2 * n + i - 1] * xm;
+  if (i < n - 1) y += bands[n + i] * xp;
+  return y;
+}
+
+__device__ __forceinline__ double circ3(const double* th, double xm, double x0, double xp) {
+  return th[1] * xm + th[0] * x0 + th[1] * xp;
+}
+
+template <int GEOM, int KIN, int RB>
+__global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p) {
+  constexpr bool D3 = GEOM >= 2;
+  constexpr unsigned FULL = 0xffffffffu;
+  if (p.step && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *p.step += 1;
+  const int nl = D3 ? p.n3 : p.n2;  // contiguous extent
+  const int n1 = p.n1;              // walked extent
+  const int l = threadIdx.x;
+  const int lane = l & 31;
+  const bool act = l < nl;
+  const int lc = act ? l : nl - 1;
+  const int i0 = blockIdx.x * RB;
+  const int j = D3 ? (int)blockIdx.y : 0;
+  const int b = blockIdx.z;
+  const long long rs = D3 ? (long long)p.n2 * p.n3 : (long long)p.n2;  // walked stride
+  const long long run_base = (long long)b * p.ncomp * p.npts + (long long)j * (D3 ? p.n3 : 0);
+  const bool periodic_walk = (GEOM == 1);
+  const bool periodic_row = (GEOM == 0);
+  const int nC = (KIN == KIN_EXTERNAL) ? p.ncomp : 2;
+  if (i0 >= n1) return;
+  const int iend = min(n1, i0 + RB);
+
+  // contiguous-axis neighbours of the value x0 held at column l of row `rowp`
+  auto row_nb = [&](const double* rowp, double x0, double& xl, double& xr) {
+    const double up = __shfl_up_sync(FULL, x0, 1);
+    const double dn = __shfl_down_sync(FULL, x0, 1);
+    int li = lc - 1, ri = lc + 1;
+    if (periodic_row) {
+      if (li < 0) li = nl - 1;
+      if (ri >= nl) ri = 0;
+    }
+    xl = (lane > 0 && li == lc - 1) ? up : ((li >= 0) ? __ldg(rowp + li) : 0.0);
+    xr = (lane < 31 && ri == lc + 1 && ri < nl) ? dn : ((ri < nl) ? __ldg(rowp + ri) : 0.0);
+  };
+
+  auto diffusion = [&](int c, int i, const double* rowp, const Win& w) -> double {
+    double xl, xr;
+    row_nb(rowp, w.c, xl, xr);
+    if (GEOM == 0) {
+      const double r = tri3(p.rho_b + (long long)c * 3 * n1, n1, i, w.m, w.c, w.p);
+      const double q = circ3(p.th + 2 * c, xl, w.c, xr);
+      return r + p.d_rho[c * n1 + i] * q;
+    } else if (GEOM == 1) {
+      const double q = circ3(p.th + 2 * c, w.m, w.c, w.p);
+      const double r = tri3(p.phi_b + (long long)c * 3 * nl, nl, lc, xl, w.c, xr);
+      return q * p.d_phi[c * nl + lc] + r;
+    } else {
+      const int jm = (j == 0) ? p.n2 - 1 : j - 1;
+      const int jp = (j == p.n2 - 1) ? 0 : j + 1;
+      const double ym = __ldg(rowp + (long long)(jm - j) * nl + lc);
+      const double yp = __ldg(rowp + (long long)(jp - j) * nl + lc);
+      const double r = tri3(p.rho_b + (long long)c * 3 * n1, n1, i, w.m, w.c, w.p);
+      const double q = circ3(p.th + 2 * c, ym, w.c, yp);
+      const double dr = p.d_rho[c * n1 + i];
+      if (GEOM == 2) {
+        const double ph = tri3(p.phi_b + (long long)c * 3 * nl, nl, lc, xl, w.c, xr);
+        return r + (dr * q) * p.d_phi[c * nl + lc] + dr * ph;
+      } else {
+        const double z = tri3(p.z_b + (long long)c * 3 * nl, nl, lc, xl, w.c, xr);
+        return r + dr * q + z;
+      }
+    }
+  };
+
+  auto win_start = [&](const double* X) -> Win {
+    Win w;
+    const int im = (i0 > 0) ? i0 - 1 : (periodic_walk ? n1 - 1 : -1);
+    w.m = (im >= 0) ? __ldg(X + (long long)im * rs + lc) : 0.0;
+    w.c = __ldg(X + (long long)i0 * rs + lc);
+    w.p = 0.0;
+    return w;
+  };
+  auto win_next = [&](const double* X, int i) -> double {
+    int ip = i + 1;
+    if (ip >= n1) ip = periodic_walk ? 0 : -1;
+    return (ip >= 0) ? __ldg(X + (long long)ip * rs + lc) : 0.0;
+  };
+
+  if (KIN == KIN_EXTERNAL) {
+    for (int c = 0; c < nC; ++c) {
+      const double* X = p.W + run_base + (long long)c * p.npts;
+      Win w = win_start(X);
+      for (int i = i0; i < iend; ++i) {
+        w.p = win_next(X, i);
+        const double* rowp = X + (long long)i * rs;
+        double val = 0.0;
+        if (p.with_diffusion) val = p.coeff[c] * diffusion(c, i, rowp, w);
+        const long long idx = run_base + (long long)c * p.npts + (long long)i * rs + lc;
+        if (p.with_reaction) val = p.with_diffusion ? __dadd_rn(val, __ldg(p.G + idx)) : __ldg(p.G + idx);
+        if (act) p.F[idx] = val;
+        w.m = w.c;
+        w.c = w.p;
+      }
+    }
+  } else {
+    const double* U = p.W + run_base;
+    const double* V = U + p.npts;
+    const double* kin = p.kin + (long long)b * p.nparams;
+    Win wu = win_start(U), wv = win_start(V);
+    for (int i = i0; i < iend; ++i) {
+      wu.p = win_next(U, i);
+      wv.p = win_next(V, i);
+      const long long off = (long long)i * rs + lc;
+      double g0 = 0.0, g1 = 0.0;
+      if (p.with_reaction) {
+        double u = wu.c, v = wv.c;
+        if (p.lift[0] != 0.0) u = __dadd_rn(u, p.lift[0]);
+        if (p.lift[1] != 0.0) v = __dadd_rn(v, p.lift[1]);
+        reaction<KIN>(kin, u, v, g0, g1);
+      }
+      double fu = g0, fv = g1;
+      if (p.with_diffusion) {
+        const double du = p.coeff[0] * diffusion(0, i, U + (long long)i * rs, wu);
+        const double dv = p.coeff[1] * diffusion(1, i, V + (long long)i * rs, wv);
+        fu = p.with_reaction ? __dadd_rn(du, g0) : du;
+        fv = p.with_reaction ? __dadd_rn(dv, g1) : dv;
+      }
+      if (act) {
+        p.F[run_base + off] = fu;
+        p.F[run_base + p.npts + off] = fv;
+      }
+      wu.m = wu.c;
+      wu.c = wu.p;
+      wv.m = wv.c;
+      wv.c = wv.p;
+    }
+  }
+}
+
+// grid = (ceil(npts / 256), batch): one thread per grid point of one run,
+// consecutive threads along the contiguous axis; 32-bit index math only.
 template <int GEOM, int KIN>
 __global__ void __launch_bounds__(256) fbuild_kernel(const StencilParams p) {
-  if (p.step && blockIdx.x == 0 && threadIdx.x == 0) *p.step += 1;
-  const long long total = p.npts * p.batch;
-  for (long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x; gid < total;
-       gid += (long long)gridDim.x * blockDim.x) {
-    const long long b = gid / p.npts;
-    const long long pt = gid - b * p.npts;
+  if (p.step && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *p.step += 1;
+  const int npts = (int)p.npts;
+  const int pt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (pt < npts) {
     int i, j, l;
     if (GEOM == 0 || GEOM == 1) {
-      j = (int)(pt % p.n2);
-      i = (int)(pt / p.n2);
+      i = pt / p.n2;
+      j = pt - i * p.n2;
       l = 0;
     } else {
-      l = (int)(pt % p.n3);
-      const long long r = pt / p.n3;
-      j = (int)(r % p.n2);
-      i = (int)(r / p.n2);
+      const int r = pt / p.n3;
+      l = pt - r * p.n3;
+      i = r / p.n2;
+      j = r - i * p.n2;
     }
-    const long long fb = b * p.ncomp * p.npts;
+    const long long fb = (long long)b * p.ncomp * p.npts;
     double g0 = 0.0, g1 = 0.0;
     if (KIN != KIN_EXTERNAL && p.with_reaction) {
       double u = __ldg(p.W + fb + pt);
