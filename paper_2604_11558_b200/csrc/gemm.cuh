@@ -80,17 +80,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
   uint64_t* empty = full + STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // tile decode: bid -> (batch item, m tile, n tile), n fastest
-  int bid = blockIdx.x;
-  const int tn = bid % p.tiles_n;
-  bid /= p.tiles_n;
-  const int tm = bid % p.tiles_m;
-  const int t = bid / p.tiles_m;
-  const int f = t / p.nslab, s = t - f * p.nslab;
-  const int c = f % p.ncomp;
-  const int m0 = tm * BM, n0 = tn * BN;
   const int KT = (p.K + 15) >> 4;
+  const int ntiles = p.nbatch * p.tiles_m * p.tiles_n;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -101,25 +92,41 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
   }
   __syncthreads();
 
+  // Persistent static schedule: CTA b takes tiles b, b + grid, ...; tile ->
+  // (batch item, m tile, n tile) with n fastest so neighbouring CTAs share the
+  // A rows in L2.  The stage ring runs continuously across tiles, so the
+  // producer streams the next tile's operands while consumers run the
+  // epilogue of the current one.
   if (warp == NCW) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       tma_prefetch_desc(&mapA);
       tma_prefetch_desc(&mapB);
-      for (int kt = 0; kt < KT; ++kt) {
-        const int st = kt % STAGES;
-        if (kt >= STAGES) mbar_wait(&empty[st], ((kt / STAGES) - 1) & 1);
-        uint8_t* sa = smem + st * STAGE;
-        uint8_t* sb = sa + SA;
-        mbar_arrive_expect_tx(&full[st], STAGE);
-        if (VAR == VAR_TN) {
-          tma_load_3d(sa, &mapA, &full[st], kt * 16, m0, f);
-          tma_load_3d(sb, &mapB, &full[st], kt * 16, n0, c);
-        } else {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int r = tile;
+        const int tn = r % p.tiles_n;
+        r /= p.tiles_n;
+        const int tm = r % p.tiles_m;
+        const int t = r / p.tiles_m;
+        const int f = t / p.nslab, s = t - f * p.nslab;
+        const int c = f % p.ncomp;
+        const int m0 = tm * BM, n0 = tn * BN;
+        for (int kt = 0; kt < KT; ++kt, ++it) {
+          const int st = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
+          uint8_t* sa = smem + st * STAGE;
+          uint8_t* sb = sa + SA;
+          mbar_arrive_expect_tx(&full[st], STAGE);
+          if (VAR == VAR_TN) {
+            tma_load_3d(sa, &mapA, &full[st], kt * 16, m0, f);
+            tma_load_3d(sb, &mapB, &full[st], kt * 16, n0, c);
+          } else {
 #pragma unroll
-          for (int q = 0; q < BM / 16; ++q) tma_load_3d(sa + q * 2048, &mapA, &full[st], m0 + 16 * q, kt * 16, c);
+            for (int q = 0; q < BM / 16; ++q) tma_load_3d(sa + q * 2048, &mapA, &full[st], m0 + 16 * q, kt * 16, c);
 #pragma unroll
-          for (int q = 0; q < BN / 16; ++q) tma_load_4d(sb + q * 2048, &mapB, &full[st], n0 + 16 * q, kt * 16, s, f);
+            for (int q = 0; q < BN / 16; ++q) tma_load_4d(sb + q * 2048, &mapB, &full[st], n0 + 16 * q, kt * 16, s, f);
+          }
         }
       }
     }
@@ -130,146 +137,158 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
   const int wy = warp / WARPS_N, wx = warp % WARPS_N;
   const int wm0 = wy * WM, wn0 = wx * WN;
   const int g = lane >> 2, tq = lane & 3;
+  int step_now = 0;
+  if (EPI == EPI_AXPY) step_now = *p.step;
+  int it = 0;
 
-  double acc[MT][NT][2];
-#pragma unroll
-  for (int i = 0; i < MT; ++i)
-#pragma unroll
-    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int r = tile;
+    const int tn = r % p.tiles_n;
+    r /= p.tiles_n;
+    const int tm = r % p.tiles_m;
+    const int t = r / p.tiles_m;
+    const int f = t / p.nslab, s = t - f * p.nslab;
+    const int c = f % p.ncomp;
+    const int m0 = tm * BM, n0 = tn * BN;
 
-  for (int kt = 0; kt < KT; ++kt) {
-    const int st = kt % STAGES;
-    mbar_wait(&full[st], (kt / STAGES) & 1);
-    const double* sa = reinterpret_cast<const double*>(smem + st * STAGE);
-    const double* sb = reinterpret_cast<const double*>(smem + st * STAGE + SA);
-    if (VAR == VAR_TN) {
-      const int pg = perm8(g);
+    double acc[MT][NT][2];
 #pragma unroll
-      for (int kk = 0; kk < 16; kk += 4) {
-        const int col = kk + tq;
-        const int off = ((((col >> 1) ^ pg)) << 1) | (col & 1);
-        double a[MT], b[NT];
+    for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int i = 0; i < MT; ++i) a[i] = sa[(wm0 + i * 8 + pg) * 16 + off];
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int kt = 0; kt < KT; ++kt, ++it) {
+      const int st = it % STAGES;
+      mbar_wait(&full[st], (it / STAGES) & 1);
+      const double* sa = reinterpret_cast<const double*>(smem + st * STAGE);
+      const double* sb = reinterpret_cast<const double*>(smem + st * STAGE + SA);
+      if (VAR == VAR_TN) {
+        const int pg = perm8(g);
 #pragma unroll
-        for (int j = 0; j < NT; ++j) b[j] = sb[(wn0 + j * 8 + pg) * 16 + off];
-#pragma unroll
-        for (int i = 0; i < MT; ++i)
-#pragma unroll
-          for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-      }
-    } else {
-#pragma unroll
-      for (int k8 = 0; k8 < 16; k8 += 8) {
-#pragma unroll
-        for (int sub = 0; sub < 2; ++sub) {
-          const int k = k8 + 2 * tq + sub;
-          const int kx = k & 7;
+        for (int kk = 0; kk < 16; kk += 4) {
+          const int col = kk + tq;
+          const int off = ((((col >> 1) ^ pg)) << 1) | (col & 1);
           double a[MT], b[NT];
 #pragma unroll
-          for (int i = 0; i < MT; ++i) {
-            const int m = wm0 + i * 8 + g;
-            const int mm = m & 15;
-            a[i] = sa[(m >> 4) * 256 + k * 16 + ((((mm >> 1) ^ kx)) << 1) + (mm & 1)];
-          }
+          for (int i = 0; i < MT; ++i) a[i] = sa[(wm0 + i * 8 + pg) * 16 + off];
 #pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            const int n = wn0 + j * 8 + g;
-            const int nn = n & 15;
-            b[j] = sb[(n >> 4) * 256 + k * 16 + ((((nn >> 1) ^ kx)) << 1) + (nn & 1)];
-          }
+          for (int j = 0; j < NT; ++j) b[j] = sb[(wn0 + j * 8 + pg) * 16 + off];
 #pragma unroll
           for (int i = 0; i < MT; ++i)
 #pragma unroll
             for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
         }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-  }
-
-  // ---------------- fused epilogue ----------------
-  int col_in8;
-  if (VAR == VAR_TN) {
-    // thread holds cols perm8(2t), perm8(2t+1) = {0,2},{4,6},{1,3},{5,7};
-    // swap with lane^2 so each thread owns an adjacent pair.
+      } else {
 #pragma unroll
-    for (int i = 0; i < MT; ++i)
+        for (int k8 = 0; k8 < 16; k8 += 8) {
 #pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        const bool hi = (tq & 2) != 0;
-        const double send = hi ? acc[i][j][0] : acc[i][j][1];
-        const double recv = __shfl_xor_sync(0xffffffffu, send, 2);
-        if (hi)
-          acc[i][j][0] = recv;
-        else
-          acc[i][j][1] = recv;
-      }
-    col_in8 = ((tq & 1) << 2) | (tq & 2);
-  } else {
-    col_in8 = 2 * tq;
-  }
-  const int row_in8 = (VAR == VAR_TN) ? perm8(g) : g;
-
-  const long long base = (long long)f * p.out_f + (long long)s * p.out_s;
-  bool bad = false;
-  int step_now = 0;
-  if (EPI == EPI_AXPY) step_now = *p.step;
-  // Gather the epilogue operands (W pair or two phi1 values per accumulator
-  // pair) for a group of EC fragment rows with all loads in flight at once,
-  // then combine and store: load latency is paid once per group instead of
-  // once per fragment.  EC < MT bounds the registers at 2+ CTAs per SM.
-  constexpr int EC = (MINB >= 2 && MT > 2) ? MT / 2 : MT;
+          for (int sub = 0; sub < 2; ++sub) {
+            const int k = k8 + 2 * tq + sub;
+            const int kx = k & 7;
+            double a[MT], b[NT];
 #pragma unroll
-  for (int i0 = 0; i0 < MT; i0 += EC) {
-    double2 opnd[EC][NT];
-    if (EPI != EPI_STORE) {
+            for (int i = 0; i < MT; ++i) {
+              const int m = wm0 + i * 8 + g;
+              const int mm = m & 15;
+              a[i] = sa[(m >> 4) * 256 + k * 16 + ((((mm >> 1) ^ kx)) << 1) + (mm & 1)];
+            }
 #pragma unroll
-      for (int ii = 0; ii < EC; ++ii) {
-        int m = m0 + wm0 + (i0 + ii) * 8 + row_in8;
-        if (m >= p.M) m = 0;
-        const double* phirow = nullptr;
-        if (EPI == EPI_PHI) phirow = p.phi + c * p.phi_c + s * p.phi_s + (long long)(m / p.phi_rdiv) * p.phi_m;
+            for (int j = 0; j < NT; ++j) {
+              const int n = wn0 + j * 8 + g;
+              const int nn = n & 15;
+              b[j] = sb[(n >> 4) * 256 + k * 16 + ((((nn >> 1) ^ kx)) << 1) + (nn & 1)];
+            }
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          int n = n0 + wn0 + j * 8 + col_in8;
-          if (n >= p.N) n = 0;
-          if (EPI == EPI_PHI) {
-            opnd[ii][j].x = __ldg(phirow + (long long)n * p.phi_n);
-            opnd[ii][j].y = __ldg(phirow + (long long)(n + 1) * p.phi_n);
-          } else {
-            opnd[ii][j] = __ldg(reinterpret_cast<const double2*>(p.w + base + (long long)m * p.ldc + n));
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+              for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
           }
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
     }
+
+    // ---------------- fused epilogue ----------------
+    int col_in8;
+    if (VAR == VAR_TN) {
+      // thread holds cols perm8(2t), perm8(2t+1) = {0,2},{4,6},{1,3},{5,7};
+      // swap with lane^2 so each thread owns an adjacent pair.
 #pragma unroll
-    for (int ii = 0; ii < EC; ++ii) {
-      const int i = i0 + ii;
-      const int m = m0 + wm0 + i * 8 + row_in8;
-      if (m >= p.M) continue;
+      for (int i = 0; i < MT; ++i)
 #pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        const int n = n0 + wn0 + j * 8 + col_in8;
-        if (n >= p.N) continue;
-        const long long idx = base + (long long)m * p.ldc + n;
-        double v0 = acc[i][j][0], v1 = acc[i][j][1];
-        if (EPI == EPI_PHI) {
-          v0 *= opnd[ii][j].x;
-          v1 *= opnd[ii][j].y;
-        } else if (EPI == EPI_AXPY) {
-          // W + tau*T rounded as the reference rounds it (no FMA contraction)
-          v0 = __dadd_rn(opnd[ii][j].x, __dmul_rn(p.tau, v0));
-          v1 = __dadd_rn(opnd[ii][j].y, __dmul_rn(p.tau, v1));
-          bad |= !(fabs(v0) <= p.limit) || !(fabs(v1) <= p.limit);
+        for (int j = 0; j < NT; ++j) {
+          const bool hi = (tq & 2) != 0;
+          const double send = hi ? acc[i][j][0] : acc[i][j][1];
+          const double recv = __shfl_xor_sync(0xffffffffu, send, 2);
+          if (hi)
+            acc[i][j][0] = recv;
+          else
+            acc[i][j][1] = recv;
         }
-        *reinterpret_cast<double2*>(p.out + idx) = make_double2(v0, v1);
+      col_in8 = ((tq & 1) << 2) | (tq & 2);
+    } else {
+      col_in8 = 2 * tq;
+    }
+    const int row_in8 = (VAR == VAR_TN) ? perm8(g) : g;
+
+    const long long base = (long long)f * p.out_f + (long long)s * p.out_s;
+    bool bad = false;
+    // Gather the epilogue operands (W pair or two phi1 values per accumulator
+    // pair) for a group of EC fragment rows with all loads in flight at once,
+    // then combine and store: load latency is paid once per group instead of
+    // once per fragment.  EC < MT bounds the registers at 2+ CTAs per SM.
+    constexpr int EC = (MINB >= 2 && MT > 2) ? MT / 2 : MT;
+#pragma unroll
+    for (int i0 = 0; i0 < MT; i0 += EC) {
+      double2 opnd[EC][NT];
+      if (EPI != EPI_STORE) {
+#pragma unroll
+        for (int ii = 0; ii < EC; ++ii) {
+          int m = m0 + wm0 + (i0 + ii) * 8 + row_in8;
+          if (m >= p.M) m = 0;
+          const double* phirow = nullptr;
+          if (EPI == EPI_PHI) phirow = p.phi + c * p.phi_c + s * p.phi_s + (long long)(m / p.phi_rdiv) * p.phi_m;
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            int n = n0 + wn0 + j * 8 + col_in8;
+            if (n >= p.N) n = 0;
+            if (EPI == EPI_PHI) {
+              opnd[ii][j].x = __ldg(phirow + (long long)n * p.phi_n);
+              opnd[ii][j].y = __ldg(phirow + (long long)(n + 1) * p.phi_n);
+            } else {
+              opnd[ii][j] = __ldg(reinterpret_cast<const double2*>(p.w + base + (long long)m * p.ldc + n));
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int ii = 0; ii < EC; ++ii) {
+        const int i = i0 + ii;
+        const int m = m0 + wm0 + i * 8 + row_in8;
+        if (m >= p.M) continue;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int n = n0 + wn0 + j * 8 + col_in8;
+          if (n >= p.N) continue;
+          const long long idx = base + (long long)m * p.ldc + n;
+          double v0 = acc[i][j][0], v1 = acc[i][j][1];
+          if (EPI == EPI_PHI) {
+            v0 *= opnd[ii][j].x;
+            v1 *= opnd[ii][j].y;
+          } else if (EPI == EPI_AXPY) {
+            // W + tau*T rounded as the reference rounds it (no FMA contraction)
+            v0 = __dadd_rn(opnd[ii][j].x, __dmul_rn(p.tau, v0));
+            v1 = __dadd_rn(opnd[ii][j].y, __dmul_rn(p.tau, v1));
+            bad |= !(fabs(v0) <= p.limit) || !(fabs(v1) <= p.limit);
+          }
+          *reinterpret_cast<double2*>(p.out + idx) = make_double2(v0, v1);
+        }
       }
     }
-  }
-  if (EPI == EPI_AXPY) {
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(p.first_bad + f, step_now);
+    if (EPI == EPI_AXPY) {
+      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(p.first_bad + f, step_now);
+    }
   }
 }
 

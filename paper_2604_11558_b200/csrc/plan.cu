@@ -105,14 +105,22 @@ int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams
                   bool configure_only) {
   auto kern = gemm_f64_kernel<VAR, BM, BN, WM, WN, ST, EPI, MINB>;
   constexpr int smem = gemm_smem_bytes<BM, BN, ST>();
+  constexpr int threads = (BM / WM) * (BN / WN) * 32 + 32;
+  static int resident = 0;  // CTAs of this instantiation that fit on the chip at once
   if (configure_only) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int per_sm = 0, dev = 0, sms = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    resident = (per_sm > 0 ? per_sm : 1) * sms;
     return CG_OK;
   }
-  const long long blocks = (long long)p.nbatch * p.tiles_m * p.tiles_n;
-  if (blocks <= 0) return CG_OK;
-  if (blocks > INT_MAX) return fail(CG_EUNSUPPORTED, "grid too large");
-  constexpr int threads = (BM / WM) * (BN / WN) * 32 + 32;
+  const long long tiles = (long long)p.nbatch * p.tiles_m * p.tiles_n;
+  if (tiles <= 0) return CG_OK;
+  if (tiles > INT_MAX) return fail(CG_EUNSUPPORTED, "grid too large");
+  // persistent grid: at most one wave of resident CTAs, each looping over tiles
+  const long long blocks = (resident > 0 && tiles > resident) ? resident : tiles;
   kern<<<(unsigned)blocks, threads, smem, stream>>>(ma, mb, p);
   CUDA_TRY(cudaGetLastError());
   return CG_OK;

@@ -256,11 +256,15 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
       }
     }
   } else {
-    const double* U = p.W + run_base;
-    const double* V = U + p.npts;
+    const double* __restrict__ U = p.W + run_base;
+    const double* __restrict__ V = U + p.npts;
+    double* __restrict__ Fo = p.F;
     const double* kin = p.kin + (long long)b * p.nparams;
     Win wu = win_start(U), wv = win_start(V);
-    for (int i = i0; i < iend; ++i) {
+#pragma unroll
+    for (int ii = 0; ii < RB; ++ii) {
+      const int i = i0 + ii;
+      if (i >= iend) break;
       wu.p = win_next(U, i);
       wv.p = win_next(V, i);
       const long long off = (long long)i * rs + lc;
@@ -279,8 +283,8 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
         fv = p.with_reaction ? __dadd_rn(dv, g1) : dv;
       }
       if (act) {
-        p.F[run_base + off] = fu;
-        p.F[run_base + p.npts + off] = fv;
+        Fo[run_base + off] = fu;
+        Fo[run_base + p.npts + off] = fv;
       }
       wu.m = wu.c;
       wu.c = wu.p;
