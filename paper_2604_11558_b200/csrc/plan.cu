@@ -155,38 +155,44 @@ int launch_gemm(int var, int epi, int cfg, const CUtensorMap& ma, const CUtensor
 __global__ void set_step_kernel(int* step, int value) { *step = value; }
 
 template <int GEOM, int KIN>
-int launch_fbuild_t(const StencilParams& p, cudaStream_t s) {
+int launch_fbuild_t(const StencilParams& p, cudaStream_t s, bool configure_only) {
+  using S = FbuildShape<GEOM>;
+  if (configure_only) {  // at plan creation, never under stream capture
+    CUDA_TRY(cudaFuncSetAttribute(fbuild_rows_kernel<GEOM, KIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024));
+    return CG_OK;
+  }
   if (p.batch > 65535) return fail(CG_EUNSUPPORTED, "batch > 65535 runs per plan");
-  const bool d3 = GEOM >= 2;
-  const int nl = d3 ? p.n3 : p.n2;
+  const int nl = S::D3 ? p.n3 : p.n2;
   if (nl > 512) return fail(CG_EUNSUPPORTED, "contiguous axis longer than 512");
-  constexpr int RB = 8;
-  const dim3 grid((unsigned)((p.n1 + RB - 1) / RB), d3 ? (unsigned)p.n2 : 1u, (unsigned)p.batch);
+  const size_t smem = (size_t)(KIN == KIN_EXTERNAL ? 1 : 2) * S::ROWS * nl * sizeof(double);
+  if (smem > 200 * 1024) return fail(CG_EUNSUPPORTED, "F-build tile exceeds shared memory");
+  const dim3 grid((unsigned)((p.n1 + S::RB - 1) / S::RB), S::D3 ? (unsigned)p.n2 : 1u, (unsigned)p.batch);
   const unsigned threads = (unsigned)((nl + 31) / 32 * 32);
-  fbuild_rows_kernel<GEOM, KIN, RB><<<grid, threads, 0, s>>>(p);
+  fbuild_rows_kernel<GEOM, KIN><<<grid, threads, smem, s>>>(p);
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
 }
 
 template <int GEOM>
-int launch_fbuild_g(int kin, const StencilParams& p, cudaStream_t s) {
+int launch_fbuild_g(int kin, const StencilParams& p, cudaStream_t s, bool conf) {
   switch (kin) {
-    case KIN_SCHNAKENBERG: return launch_fbuild_t<GEOM, KIN_SCHNAKENBERG>(p, s);
-    case KIN_BRUSSELATOR: return launch_fbuild_t<GEOM, KIN_BRUSSELATOR>(p, s);
-    case KIN_GRAY_SCOTT: return launch_fbuild_t<GEOM, KIN_GRAY_SCOTT>(p, s);
-    case KIN_BVAM_ETA: return launch_fbuild_t<GEOM, KIN_BVAM_ETA>(p, s);
-    case KIN_BVAM: return launch_fbuild_t<GEOM, KIN_BVAM>(p, s);
-    case KIN_DIB: return launch_fbuild_t<GEOM, KIN_DIB>(p, s);
-    default: return launch_fbuild_t<GEOM, KIN_EXTERNAL>(p, s);
+    case KIN_SCHNAKENBERG: return launch_fbuild_t<GEOM, KIN_SCHNAKENBERG>(p, s, conf);
+    case KIN_BRUSSELATOR: return launch_fbuild_t<GEOM, KIN_BRUSSELATOR>(p, s, conf);
+    case KIN_GRAY_SCOTT: return launch_fbuild_t<GEOM, KIN_GRAY_SCOTT>(p, s, conf);
+    case KIN_BVAM_ETA: return launch_fbuild_t<GEOM, KIN_BVAM_ETA>(p, s, conf);
+    case KIN_BVAM: return launch_fbuild_t<GEOM, KIN_BVAM>(p, s, conf);
+    case KIN_DIB: return launch_fbuild_t<GEOM, KIN_DIB>(p, s, conf);
+    default: return launch_fbuild_t<GEOM, KIN_EXTERNAL>(p, s, conf);
   }
 }
 
-int launch_fbuild(int geom, int kin, const StencilParams& p, cudaStream_t s) {
+int launch_fbuild(int geom, int kin, const StencilParams& p, cudaStream_t s, bool conf = false) {
   switch (geom) {
-    case CG_DISK: return launch_fbuild_g<0>(kin, p, s);
-    case CG_SPHERE: return launch_fbuild_g<1>(kin, p, s);
-    case CG_BALL: return launch_fbuild_g<2>(kin, p, s);
-    default: return launch_fbuild_g<3>(kin, p, s);
+    case CG_DISK: return launch_fbuild_g<0>(kin, p, s, conf);
+    case CG_SPHERE: return launch_fbuild_g<1>(kin, p, s, conf);
+    case CG_BALL: return launch_fbuild_g<2>(kin, p, s, conf);
+    default: return launch_fbuild_g<3>(kin, p, s, conf);
   }
 }
 
@@ -641,6 +647,11 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
     CUtensorMap dummy{};
     GemmParams gp{};
     if ((rc = launch_gemm(st.var, st.epi, st.cfg, dummy, dummy, gp, nullptr, true))) return bail(rc);
+  }
+  {
+    StencilParams sp{};
+    if ((rc = launch_fbuild(p->geom, KIN_EXTERNAL, sp, nullptr, true))) return bail(rc);
+    if ((rc = launch_fbuild(p->geom, p->kin, sp, nullptr, true))) return bail(rc);
   }
   const size_t bytes = (size_t)p->elems * sizeof(double);
   if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&p->X)))) return bail(rc);

@@ -40,51 +40,6 @@ struct StencilParams {
   int* step;           // incremented once per launch when non-null
 };
 
-// y = c_{i-1} x_{i-1} + a_i x_i + b_i x_{i+1} along one axis of extent n.
-__device__ __forceinline__ double tri_axis(const double* bands, int n, int i, const double* x, long long stride) {
-  const double* a = bands;
-  const double* b = bands + n;
-  const double* c = bands + 2 * n;
-  double y = a[i] * x[0];
-  if (i > 0) y += c[i - 1] * x[-stride];
-  if (i < n - 1) y += b[i] * x[stride];
-  return y;
-}
-
-// periodic: off x_{i-1} + diag x_i + off x_{i+1}
-__device__ __forceinline__ double circ_axis(const double* th, int n, int i, const double* x, long long stride) {
-  const long long dm = (i == 0) ? (long long)(n - 1) * stride : -stride;
-  const long long dp = (i == n - 1) ? -(long long)(n - 1) * stride : stride;
-  return th[1] * x[dm] + th[0] * x[0] + th[1] * x[dp];
-}
-
-template <int GEOM>
-__device__ __forceinline__ double diffusion_at(const StencilParams& p, int c, const double* x, int i, int j, int l) {
-  // x points at W[b][c][i][j][l]
-  if (GEOM == 0) {  // disk (rho, theta)
-    const double r = tri_axis(p.rho_b + (long long)c * 3 * p.n1, p.n1, i, x, p.n2);
-    const double q = circ_axis(p.th + 2 * c, p.n2, j, x, 1);
-    return r + p.d_rho[c * p.n1 + i] * q;
-  } else if (GEOM == 1) {  // sphere (theta periodic, phi polar)
-    const double q = circ_axis(p.th + 2 * c, p.n1, i, x, p.n2);
-    const double r = tri_axis(p.phi_b + (long long)c * 3 * p.n2, p.n2, j, x, 1);
-    return q * p.d_phi[c * p.n2 + j] + r;
-  } else if (GEOM == 2) {  // ball (rho, theta periodic, phi polar)
-    const long long s1 = (long long)p.n2 * p.n3;
-    const double r = tri_axis(p.rho_b + (long long)c * 3 * p.n1, p.n1, i, x, s1);
-    const double q = circ_axis(p.th + 2 * c, p.n2, j, x, p.n3);
-    const double ph = tri_axis(p.phi_b + (long long)c * 3 * p.n3, p.n3, l, x, 1);
-    const double dr = p.d_rho[c * p.n1 + i];
-    return r + (dr * q) * p.d_phi[c * p.n3 + l] + dr * ph;
-  } else {  // cylinder (rho, theta periodic, z)
-    const long long s1 = (long long)p.n2 * p.n3;
-    const double r = tri_axis(p.rho_b + (long long)c * 3 * p.n1, p.n1, i, x, s1);
-    const double q = circ_axis(p.th + 2 * c, p.n2, j, x, p.n3);
-    const double z = tri_axis(p.z_b + (long long)c * 3 * p.n3, p.n3, l, x, 1);
-    return r + p.d_rho[c * p.n1 + i] * q + z;
-  }
-}
-
 // Two-species reaction, rounded operation by operation in the reference's
 // NumPy order (no FMA contraction), so g matches the oracle bit for bit.
 template <int KIN>
@@ -137,17 +92,15 @@ __device__ __forceinline__ void reaction(const double* k, double u, double v, do
 }
 
 // ---------------------------------------------------------------------------
-// Register-blocked F-build.  Lanes run along the contiguous axis (coalesced
-// loads/stores; in-row neighbours come from warp shuffles), each thread walks
-// RB consecutive points of the first axis with a 3-value sliding window, so
-// every W value is read from memory about once (the naive one-thread-per-
-// point kernel re-read 5-7 neighbours per point and was L1-bound).
-//   grid = (ceil(n1 / RB), 3-D ? n2 : 1, batch), block = round32(n_last)
+// F-build: one CTA stages RB+2 consecutive rows of the first axis (plus, for
+// 3-D fields, the RB rows at theta-1 and theta+1) of every component into
+// shared memory with all loads in flight at once, then each thread computes
+// its column of the RB interior rows from shared memory.  Every W value is
+// read from HBM about once; loads, compute and the coalesced F stores are
+// separated so the kernel streams at HBM speed.
+//   grid = (ceil(n1 / RB), 3-D ? n2 : 1, batch), block = round32(n_last),
+//   dynamic smem = ncomp_staged * rows * n_last * 8 bytes
 // ---------------------------------------------------------------------------
-
-struct Win {
-  double m, c, p;
-};
 
 // three-point tridiagonal row: c_{i-1} x_{i-1} + a_i x_i + b_i x_{i+1}
 __device__ __forceinline__ double tri3(const double* bands, int n, int i, double xm, double x0, double xp) {
@@ -161,181 +114,140 @@ __device__ __forceinline__ double circ3(const double* th, double xm, double x0, 
   return th[1] * xm + th[0] * x0 + th[1] * xp;
 }
 
-template <int GEOM, int KIN, int RB>
-__global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p) {
-  constexpr bool D3 = GEOM >= 2;
-  constexpr unsigned FULL = 0xffffffffu;
-  if (p.step && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *p.step += 1;
-  const int nl = D3 ? p.n3 : p.n2;  // contiguous extent
-  const int n1 = p.n1;              // walked extent
-  const int l = threadIdx.x;
-  const int lane = l & 31;
-  const bool act = l < nl;
-  const int lc = act ? l : nl - 1;
-  const int i0 = blockIdx.x * RB;
-  const int j = D3 ? (int)blockIdx.y : 0;
-  const int b = blockIdx.z;
-  const long long rs = D3 ? (long long)p.n2 * p.n3 : (long long)p.n2;  // walked stride
-  const long long run_base = (long long)b * p.ncomp * p.npts + (long long)j * (D3 ? p.n3 : 0);
+template <int GEOM>
+struct FbuildShape {
+  static constexpr bool D3 = GEOM >= 2;
+  static constexpr int RB = D3 ? 4 : 8;              // interior rows per CTA
+  static constexpr int ROWS = D3 ? 3 * RB + 2 : RB + 2;  // staged rows per component
+};
+
+// stage component X's rows for this CTA into s[ROWS][nl]
+template <int GEOM>
+__device__ __forceinline__ void stage_rows(double* s, const double* __restrict__ X, int i0, int j, int n1, int n2,
+                                           int nl, long long rs) {
+  using S = FbuildShape<GEOM>;
   const bool periodic_walk = (GEOM == 1);
-  const bool periodic_row = (GEOM == 0);
-  const int nC = (KIN == KIN_EXTERNAL) ? p.ncomp : 2;
-  if (i0 >= n1) return;
-  const int iend = min(n1, i0 + RB);
-
-  // contiguous-axis neighbours of the value x0 held at column l of row `rowp`
-  auto row_nb = [&](const double* rowp, double x0, double& xl, double& xr) {
-    const double up = __shfl_up_sync(FULL, x0, 1);
-    const double dn = __shfl_down_sync(FULL, x0, 1);
-    int li = lc - 1, ri = lc + 1;
-    if (periodic_row) {
-      if (li < 0) li = nl - 1;
-      if (ri >= nl) ri = 0;
-    }
-    xl = (lane > 0 && li == lc - 1) ? up : ((li >= 0) ? __ldg(rowp + li) : 0.0);
-    xr = (lane < 31 && ri == lc + 1 && ri < nl) ? dn : ((ri < nl) ? __ldg(rowp + ri) : 0.0);
-  };
-
-  auto diffusion = [&](int c, int i, const double* rowp, const Win& w) -> double {
-    double xl, xr;
-    row_nb(rowp, w.c, xl, xr);
-    if (GEOM == 0) {
-      const double r = tri3(p.rho_b + (long long)c * 3 * n1, n1, i, w.m, w.c, w.p);
-      const double q = circ3(p.th + 2 * c, xl, w.c, xr);
-      return r + p.d_rho[c * n1 + i] * q;
-    } else if (GEOM == 1) {
-      const double q = circ3(p.th + 2 * c, w.m, w.c, w.p);
-      const double r = tri3(p.phi_b + (long long)c * 3 * nl, nl, lc, xl, w.c, xr);
-      return q * p.d_phi[c * nl + lc] + r;
-    } else {
-      const int jm = (j == 0) ? p.n2 - 1 : j - 1;
-      const int jp = (j == p.n2 - 1) ? 0 : j + 1;
-      const double ym = __ldg(rowp + (long long)(jm - j) * nl + lc);
-      const double yp = __ldg(rowp + (long long)(jp - j) * nl + lc);
-      const double r = tri3(p.rho_b + (long long)c * 3 * n1, n1, i, w.m, w.c, w.p);
-      const double q = circ3(p.th + 2 * c, ym, w.c, yp);
-      const double dr = p.d_rho[c * n1 + i];
-      if (GEOM == 2) {
-        const double ph = tri3(p.phi_b + (long long)c * 3 * nl, nl, lc, xl, w.c, xr);
-        return r + (dr * q) * p.d_phi[c * nl + lc] + dr * ph;
-      } else {
-        const double z = tri3(p.z_b + (long long)c * 3 * nl, nl, lc, xl, w.c, xr);
-        return r + dr * q + z;
-      }
-    }
-  };
-
-  auto win_start = [&](const double* X) -> Win {
-    Win w;
-    const int im = (i0 > 0) ? i0 - 1 : (periodic_walk ? n1 - 1 : -1);
-    w.m = (im >= 0) ? __ldg(X + (long long)im * rs + lc) : 0.0;
-    w.c = __ldg(X + (long long)i0 * rs + lc);
-    w.p = 0.0;
-    return w;
-  };
-  auto win_next = [&](const double* X, int i) -> double {
-    int ip = i + 1;
-    if (ip >= n1) ip = periodic_walk ? 0 : -1;
-    return (ip >= 0) ? __ldg(X + (long long)ip * rs + lc) : 0.0;
-  };
-
-  if (KIN == KIN_EXTERNAL) {
-    for (int c = 0; c < nC; ++c) {
-      const double* X = p.W + run_base + (long long)c * p.npts;
-      Win w = win_start(X);
-      for (int i = i0; i < iend; ++i) {
-        w.p = win_next(X, i);
-        const double* rowp = X + (long long)i * rs;
-        double val = 0.0;
-        if (p.with_diffusion) val = p.coeff[c] * diffusion(c, i, rowp, w);
-        const long long idx = run_base + (long long)c * p.npts + (long long)i * rs + lc;
-        if (p.with_reaction) val = p.with_diffusion ? __dadd_rn(val, __ldg(p.G + idx)) : __ldg(p.G + idx);
-        if (act) p.F[idx] = val;
-        w.m = w.c;
-        w.c = w.p;
-      }
-    }
-  } else {
-    const double* __restrict__ U = p.W + run_base;
-    const double* __restrict__ V = U + p.npts;
-    double* __restrict__ Fo = p.F;
-    const double* kin = p.kin + (long long)b * p.nparams;
-    Win wu = win_start(U), wv = win_start(V);
+  const int l = threadIdx.x;
+  if (l >= nl) return;
 #pragma unroll
-    for (int ii = 0; ii < RB; ++ii) {
-      const int i = i0 + ii;
-      if (i >= iend) break;
-      wu.p = win_next(U, i);
-      wv.p = win_next(V, i);
-      const long long off = (long long)i * rs + lc;
-      double g0 = 0.0, g1 = 0.0;
-      if (p.with_reaction) {
-        double u = wu.c, v = wv.c;
-        if (p.lift[0] != 0.0) u = __dadd_rn(u, p.lift[0]);
-        if (p.lift[1] != 0.0) v = __dadd_rn(v, p.lift[1]);
-        reaction<KIN>(kin, u, v, g0, g1);
-      }
-      double fu = g0, fv = g1;
-      if (p.with_diffusion) {
-        const double du = p.coeff[0] * diffusion(0, i, U + (long long)i * rs, wu);
-        const double dv = p.coeff[1] * diffusion(1, i, V + (long long)i * rs, wv);
-        fu = p.with_reaction ? __dadd_rn(du, g0) : du;
-        fv = p.with_reaction ? __dadd_rn(dv, g1) : dv;
-      }
-      if (act) {
-        Fo[run_base + off] = fu;
-        Fo[run_base + p.npts + off] = fv;
-      }
-      wu.m = wu.c;
-      wu.c = wu.p;
-      wv.m = wv.c;
-      wv.c = wv.p;
+  for (int r = 0; r < S::RB + 2; ++r) {
+    int i = i0 - 1 + r;
+    if (i < 0) i = periodic_walk ? n1 - 1 : 0;
+    if (i >= n1) i = periodic_walk ? i - n1 : n1 - 1;
+    s[r * nl + l] = __ldg(X + (long long)i * rs + l);
+  }
+  if (S::D3) {
+    const int jm = (j == 0) ? n2 - 1 : j - 1;
+    const int jp = (j == n2 - 1) ? 0 : j + 1;
+#pragma unroll
+    for (int r = 0; r < S::RB; ++r) {
+      const int i = min(i0 + r, n1 - 1);
+      s[(S::RB + 2 + r) * nl + l] = __ldg(X + (long long)i * rs + (long long)(jm - j) * nl + l);
+      s[(2 * S::RB + 2 + r) * nl + l] = __ldg(X + (long long)i * rs + (long long)(jp - j) * nl + l);
     }
   }
 }
 
-// grid = (ceil(npts / 256), batch): one thread per grid point of one run,
-// consecutive threads along the contiguous axis; 32-bit index math only.
+// coeff-free diffusion action at interior row r (global row i), column l
+template <int GEOM>
+__device__ __forceinline__ double diffusion_smem(const StencilParams& p, int c, const double* s, int r, int i, int j,
+                                                 int l, int nl) {
+  using S = FbuildShape<GEOM>;
+  const double xm = s[r * nl + l], x0 = s[(r + 1) * nl + l], xp = s[(r + 2) * nl + l];
+  int ll = l - 1, lr = l + 1;
+  if (GEOM == 0) {  // periodic contiguous axis
+    if (ll < 0) ll = nl - 1;
+    if (lr >= nl) lr = 0;
+  }
+  const double xl = (ll >= 0) ? s[(r + 1) * nl + ll] : 0.0;
+  const double xr = (lr < nl) ? s[(r + 1) * nl + lr] : 0.0;
+  const int n1 = p.n1;
+  if (GEOM == 0) {  // disk: rho walked (tridiagonal), theta contiguous (periodic)
+    const double rr = tri3(p.rho_b + (long long)c * 3 * n1, n1, i, xm, x0, xp);
+    const double q = circ3(p.th + 2 * c, xl, x0, xr);
+    return rr + p.d_rho[c * n1 + i] * q;
+  } else if (GEOM == 1) {  // sphere: theta walked (periodic), phi contiguous (tridiagonal)
+    const double q = circ3(p.th + 2 * c, xm, x0, xp);
+    const double rr = tri3(p.phi_b + (long long)c * 3 * nl, nl, l, xl, x0, xr);
+    return q * p.d_phi[c * nl + l] + rr;
+  } else {
+    const double ym = s[(S::RB + 2 + r) * nl + l], yp = s[(2 * S::RB + 2 + r) * nl + l];
+    const double rr = tri3(p.rho_b + (long long)c * 3 * n1, n1, i, xm, x0, xp);
+    const double q = circ3(p.th + 2 * c, ym, x0, yp);
+    const double dr = p.d_rho[c * n1 + i];
+    if (GEOM == 2) {  // ball: phi contiguous (tridiagonal)
+      const double ph = tri3(p.phi_b + (long long)c * 3 * nl, nl, l, xl, x0, xr);
+      return rr + (dr * q) * p.d_phi[c * nl + l] + dr * ph;
+    } else {  // cylinder: z contiguous (tridiagonal)
+      const double z = tri3(p.z_b + (long long)c * 3 * nl, nl, l, xl, x0, xr);
+      return rr + dr * q + z;
+    }
+  }
+}
+
 template <int GEOM, int KIN>
-__global__ void __launch_bounds__(256) fbuild_kernel(const StencilParams p) {
-  if (p.step && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *p.step += 1;
-  const int npts = (int)p.npts;
-  const int pt = blockIdx.x * blockDim.x + threadIdx.x;
-  const int b = blockIdx.y;
-  if (pt < npts) {
-    int i, j, l;
-    if (GEOM == 0 || GEOM == 1) {
-      i = pt / p.n2;
-      j = pt - i * p.n2;
-      l = 0;
-    } else {
-      const int r = pt / p.n3;
-      l = pt - r * p.n3;
-      i = r / p.n2;
-      j = r - i * p.n2;
-    }
-    const long long fb = (long long)b * p.ncomp * p.npts;
-    double g0 = 0.0, g1 = 0.0;
-    if (KIN != KIN_EXTERNAL && p.with_reaction) {
-      double u = __ldg(p.W + fb + pt);
-      double v = __ldg(p.W + fb + p.npts + pt);
-      if (p.lift[0] != 0.0) u = __dadd_rn(u, p.lift[0]);
-      if (p.lift[1] != 0.0) v = __dadd_rn(v, p.lift[1]);
-      reaction<KIN>(p.kin + b * p.nparams, u, v, g0, g1);
-    }
+__global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p) {
+  using S = FbuildShape<GEOM>;
+  extern __shared__ double fb_smem[];
+  if (p.step && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *p.step += 1;
+  const int nl = S::D3 ? p.n3 : p.n2;
+  const int n1 = p.n1;
+  const int l = threadIdx.x;
+  const int i0 = blockIdx.x * S::RB;
+  const int j = S::D3 ? (int)blockIdx.y : 0;
+  const int b = blockIdx.z;
+  const long long rs = S::D3 ? (long long)p.n2 * p.n3 : (long long)p.n2;
+  const long long run_base = (long long)b * p.ncomp * p.npts + (long long)j * (S::D3 ? p.n3 : 0);
+  const int plane = S::ROWS * nl;
+
+  if (KIN == KIN_EXTERNAL) {
     for (int c = 0; c < p.ncomp; ++c) {
-      const long long idx = fb + (long long)c * p.npts + pt;
-      double val = 0.0;
-      if (p.with_diffusion) val = p.coeff[c] * diffusion_at<GEOM>(p, c, p.W + idx, i, j, l);
-      if (p.with_reaction) {
-        double gc;
-        if (KIN == KIN_EXTERNAL)
-          gc = __ldg(p.G + idx);
-        else
-          gc = (c == 0) ? g0 : g1;
-        val = p.with_diffusion ? __dadd_rn(val, gc) : gc;
+      const double* X = p.W + run_base + (long long)c * p.npts;
+      if (c > 0) __syncthreads();
+      stage_rows<GEOM>(fb_smem, X, i0, j, n1, p.n2, nl, rs);
+      __syncthreads();
+      if (l < nl) {
+#pragma unroll
+        for (int r = 0; r < S::RB; ++r) {
+          const int i = i0 + r;
+          if (i >= n1) break;
+          const long long idx = run_base + (long long)c * p.npts + (long long)i * rs + l;
+          double val = 0.0;
+          if (p.with_diffusion) val = p.coeff[c] * diffusion_smem<GEOM>(p, c, fb_smem, r, i, j, l, nl);
+          if (p.with_reaction) val = p.with_diffusion ? __dadd_rn(val, __ldg(p.G + idx)) : __ldg(p.G + idx);
+          p.F[idx] = val;
+        }
       }
-      p.F[idx] = val;
+    }
+  } else {
+    stage_rows<GEOM>(fb_smem, p.W + run_base, i0, j, n1, p.n2, nl, rs);
+    stage_rows<GEOM>(fb_smem + plane, p.W + run_base + p.npts, i0, j, n1, p.n2, nl, rs);
+    __syncthreads();
+    if (l >= nl) return;
+    const double* kin = p.kin + (long long)b * p.nparams;
+    const double lift0 = p.lift[0], lift1 = p.lift[1];
+    double* __restrict__ Fo = p.F;
+#pragma unroll
+    for (int r = 0; r < S::RB; ++r) {
+      const int i = i0 + r;
+      if (i >= n1) break;
+      const long long off = run_base + (long long)i * rs + l;
+      double g0 = 0.0, g1 = 0.0;
+      if (p.with_reaction) {
+        double u = fb_smem[(r + 1) * nl + l], v = fb_smem[plane + (r + 1) * nl + l];
+        if (lift0 != 0.0) u = __dadd_rn(u, lift0);
+        if (lift1 != 0.0) v = __dadd_rn(v, lift1);
+        reaction<KIN>(kin, u, v, g0, g1);
+      }
+      double fu = g0, fv = g1;
+      if (p.with_diffusion) {
+        const double du = p.coeff[0] * diffusion_smem<GEOM>(p, 0, fb_smem, r, i, j, l, nl);
+        const double dv = p.coeff[1] * diffusion_smem<GEOM>(p, 1, fb_smem + plane, r, i, j, l, nl);
+        fu = p.with_reaction ? __dadd_rn(du, g0) : du;
+        fv = p.with_reaction ? __dadd_rn(dv, g1) : dv;
+      }
+      Fo[off] = fu;
+      Fo[off + p.npts] = fv;
     }
   }
 }
