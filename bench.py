@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--chunk", type=int, default=M_CONFIG, help="time steps per bench step")
     ap.add_argument("--impl", choices=["engine", "reference"], default="engine")
     ap.add_argument("--no-extras", action="store_true", help="skip per-config / CPU baseline legs")
+    ap.add_argument("--theta", choices=["fft", "gemm"], default="fft",
+                    help="periodic-theta factor as the exact FFT propagator or as two DMMA mu-mode products")
     return ap.parse_args()
 
 
@@ -174,7 +176,8 @@ def kernel_roofline(plan, state, reps=20):
             row = {"kernel": f"gemm_stage{stage}", "bound": "tensor", "achieved": flops / sec / 1e12,
                    "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "flops_per_launch": flops}
         else:
-            row = {"kernel": "fbuild", "bound": "hbm", "achieved": nbytes / sec / 1e9, "peak": hbm,
+            name = "fbuild" if stage < 0 else f"theta_fft_stage{stage}"
+            row = {"kernel": name, "bound": "hbm", "achieved": nbytes / sec / 1e9, "peak": hbm,
                    "unit": "GB/s", "bytes_per_launch": nbytes}
         row["frac"] = row["achieved"] / row["peak"]
         row["ms_per_launch"] = sec * 1e3
@@ -183,6 +186,37 @@ def kernel_roofline(plan, state, reps=20):
     for r in rows:
         r["share_of_step"] = r["ms_per_launch"] / step_ms
     return rows
+
+
+def theta_variants(ens, init_dev, chunk, stream):
+    """One bench step of config 5 under each theta mode (same inputs, same
+    timing rules) so both formulations are reported side by side."""
+    import torch
+
+    from paper_2604_11558_b200.ensemble import Ensemble
+
+    out = {}
+    for mode in ("fft", "gemm"):
+        e = Ensemble.__new__(Ensemble)
+        from paper_2604_11558_b200.ensemble import ensemble_plan
+
+        plan = ensemble_plan(ens.plan_template, "schnakenberg", ens.plan_params, TAU, theta=mode)
+        state = init_dev.clone()
+        bad = torch.full(state.shape[:2], 2**31 - 1, dtype=torch.int32, device="cuda")
+        plan.run(state, 0, 32, bad)  # warm-up (graph capture)
+        state.copy_(init_dev)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        plan.run(state, 0, chunk, bad)
+        e1.record(stream)
+        e1.synchronize()
+        sec = e0.elapsed_time(e1) / 1e3
+        out[mode] = {"value": dof_total() * chunk / sec, "ms_per_time_step": sec / chunk * 1e3}
+        plan.close()
+        del state
+        del e
+    return out
 
 
 def ncu_traffic(kernel_key):
@@ -194,7 +228,7 @@ def ncu_traffic(kernel_key):
         return None
 
 
-def per_config_gpu(k, steps=200, warmup=20):
+def per_config_gpu(k, steps=200, warmup=20, theta=None):
     """One-GPU throughput of BASELINE config k (steps/s, DOF*steps/s) and the
     GEMM chain's FP64 fraction."""
     import numpy as np
@@ -207,7 +241,7 @@ def per_config_gpu(k, steps=200, warmup=20):
     m, t_star = configs.STEPS[k]
     tau = t_star / m
     geos = [prepare(c.ops, tau) for c in system.components]
-    plan = SplitPlan(geos, 1, system.kinetics.kind, system.kinetics.param_vector()[None, :])
+    plan = SplitPlan(geos, 1, system.kinetics.kind, system.kinetics.param_vector()[None, :], theta=theta)
     init = torch.from_numpy(np.stack([c.initial for c in system.components])[None]).cuda()
     state = init.clone()
     bad = torch.full((1, 2), INT32_MAX, dtype=torch.int32, device="cuda")
@@ -224,7 +258,7 @@ def per_config_gpu(k, steps=200, warmup=20):
     flops = sum(plan.stage_info(s)[0] for s in range(plan.stage_count()))
     rows = kernel_roofline(plan, init, reps=10)
     gemm_sec = sum(r["ms_per_launch"] for r in rows if r["bound"] == "tensor") / 1e3
-    return {"config": configs.NAMES[k], "dof": dof, "ms_per_step": sec * 1e3, "steps_per_s": 1.0 / sec,
+    return {"config": configs.NAMES[k], "theta": plan.theta, "dof": dof, "ms_per_step": sec * 1e3, "steps_per_s": 1.0 / sec,
             "dof_steps_per_s": dof / sec, "gemm_flops_per_step": flops,
             "gemm_chain_frac_fp64_peak": flops / gemm_sec / 1e12 / FP64_PEAK_TFLOPS,
             "step_frac_fp64_peak": flops / sec / 1e12 / FP64_PEAK_TFLOPS}
@@ -237,6 +271,9 @@ def engine_arm(args):
     from paper_2604_11558_b200 import configs
     from paper_2604_11558_b200.ensemble import Ensemble, gather_fields, shard_range
 
+    from paper_2604_11558_b200 import integrators
+
+    integrators.THETA_MODE = args.theta
     world, rank, local = dist_setup(args)
     lo, hi = shard_range(RUNS, rank, world)
     inputs = configs.config5_inputs(lo, hi - lo)
@@ -325,6 +362,8 @@ def engine_arm(args):
                         "2 species, tau=1e-3; bench step = whole ensemble over `time_steps_per_bench_step`",
             "runs": RUNS, "grid": list(DIMS), "species": NCOMP, "tau": TAU,
             "time_steps_per_bench_step": chunk, "dof": dof_total(),
+            "theta": args.theta + (" (exact real-FFT propagator for Q diag(Phi) Q^T)" if args.theta == "fft"
+                                   else " (two DMMA mu-mode products, the reference's factorisation)"),
             "parallelism": f"ensemble shards over {world} GPU(s), no data-path collective",
             "l2": "state 268 MB/GPU at N=1 exceeds 126 MB L2; 256 MB L2 flush between timed bench steps",
         },
@@ -348,7 +387,8 @@ def engine_arm(args):
         line["clocks"] = cl
     if world == 1 and not args.no_extras:
         line["cpu_baseline"] = cpu_baseline_ensemble(sample_steps=200)
-        line["per_config"] = [per_config_gpu(k) for k in (1, 2, 3, 4)]
+        line["per_config"] = [per_config_gpu(k, theta=t) for k in (1, 2, 3, 4) for t in ("fft", "gemm")]
+        line["variants"] = theta_variants(ens, init_dev, chunk, stream)
         line["per_config_cpu"] = cpu_per_config()
     print(json.dumps(line), flush=True)
     if world > 1:

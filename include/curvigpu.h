@@ -118,7 +118,13 @@ typedef struct {
   int nparams;
   const double* kin_params; /* [batch][nparams] */
   const double* lift;     /* [ncomp] constant lift restoring physical values */
+  int options;            /* CG_OPT_* bit set */
 } cg_desc;
+
+/* options: apply the periodic-theta pair Q_theta diag(Phi) Q_theta^T as an
+ * exact real-FFT propagator (power-of-two n_theta) instead of two dense DMMA
+ * mu-mode products; same mathematics (integrators.py:204-206 etc.), O(n log n). */
+#define CG_OPT_THETA_FFT 1
 
 int cg_plan_create(const cg_desc* desc, cg_plan** out);
 void cg_plan_destroy(cg_plan* plan);

@@ -20,6 +20,7 @@ CG_ECUDA = -2
 CG_EUNSUPPORTED = -3
 
 GEOMETRY_CODES = {"disk": 0, "sphere": 1, "ball": 2, "cylinder": 3}
+CG_OPT_THETA_FFT = 1
 
 
 class EngineError(RuntimeError):
@@ -53,6 +54,7 @@ class cg_desc(ctypes.Structure):
         ("nparams", ctypes.c_int),
         ("kin_params", _dp),
         ("lift", _dp),
+        ("options", ctypes.c_int),
     ]
 
 

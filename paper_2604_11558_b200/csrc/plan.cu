@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -21,6 +22,7 @@
 #include "curvigpu.h"
 #include "gemm.cuh"
 #include "stencil.cuh"
+#include "thetafft.cuh"
 
 using namespace cg;
 
@@ -202,6 +204,8 @@ int launch_fbuild(int geom, int kin, const StencilParams& p, cudaStream_t s, boo
 
 enum { BUF_X = 0, BUF_Y = 1, BUF_OUT = 2 };
 
+constexpr int VAR_THETA = 2;  // FFT theta propagator (thetafft.cuh), not a GEMM
+
 struct Stage {
   int var, epi, cfg;
   int M, N, K, nslab;
@@ -210,6 +214,10 @@ struct Stage {
   long long phi_c, phi_s;
   int phi_m, phi_n, phi_rdiv;
   CUtensorMap opmap;  // operator operand (B for TN, A for NN)
+  // VAR_THETA: field = [A][N][Bc], W lines per CTA, Phi_j table, twiddles
+  int tA, tBc, tW, tclass_mode, tnclass;
+  const double* phif;
+  const double2* tw;
 };
 
 struct GraphEntry {
@@ -329,6 +337,53 @@ int add_stage(cg_plan* p, int var, int epi, int M, int N, int K, int nslab, int 
 
 double* buf_ptr(cg_plan* p, int id, double* out) { return id == BUF_X ? p->X : id == BUF_Y ? p->Y : out; }
 
+bool pow2(int n) { return n >= 4 && (n & (n - 1)) == 0; }
+
+// FFT theta-propagator stage over fields viewed as [A][N][Bc].  phi_at(c, cls,
+// col) returns Phi for component c, line class cls and eigen-column col; the
+// kernel takes Phi_j = Phi[col(j)] per frequency j = 0..N/2.
+template <typename PhiAt>
+int add_theta_stage(cg_plan* p, int epi, int src, int dst, int N, int A, int Bc, int class_mode, int nclass,
+                    PhiAt phi_at) {
+  Stage st{};
+  st.var = VAR_THETA;
+  st.epi = epi;
+  st.N = N;
+  st.src = src;
+  st.dst = dst;
+  st.tA = A;
+  st.tBc = Bc;
+  st.tclass_mode = class_mode;
+  st.tnclass = nclass;
+  const int M = N / 2;
+  const int span = (Bc == 1) ? A : Bc;
+  int W = 16;
+  while (W > 1 && (span % W != 0 || theta_smem_bytes(N, W) > 96 * 1024)) W /= 2;
+  st.tW = W;
+  std::vector<double> h((size_t)p->C * nclass * (M + 1));
+  for (int c = 0; c < p->C; ++c)
+    for (int cls = 0; cls < nclass; ++cls)
+      for (int j = 0; j <= M; ++j) {
+        const int col = (j == 0) ? 0 : (j == M ? N - 1 : 2 * j - 1);
+        h[((size_t)c * nclass + cls) * (M + 1) + j] = phi_at(c, cls, col);
+      }
+  double* phif = nullptr;
+  int rc = upload(p, h.data(), h.size(), &phif);
+  if (rc) return rc;
+  std::vector<double> tw(2 * (size_t)N);
+  for (int t = 0; t < N; ++t) {
+    const double ang = 2.0 * M_PI * (double)t / (double)N;
+    tw[2 * t] = std::cos(ang);
+    tw[2 * t + 1] = -std::sin(ang);
+  }
+  double* twd = nullptr;
+  if ((rc = upload(p, tw.data(), tw.size(), &twd))) return rc;
+  st.phif = phif;
+  st.tw = reinterpret_cast<const double2*>(twd);
+  p->stages.push_back(st);
+  return CG_OK;
+}
+
 int launch_fstage(cg_plan* p, const double* Win, const double* Gext, bool fused_kin, bool count_step,
                   cudaStream_t s) {
   StencilParams sp{};
@@ -358,8 +413,60 @@ int launch_fstage(cg_plan* p, const double* Win, const double* Gext, bool fused_
   return launch_fbuild(p->geom, fused_kin ? p->kin : KIN_EXTERNAL, sp, s);
 }
 
+int launch_theta(cg_plan* p, const Stage& st, const double* Win, double* Wout, int* first_bad, cudaStream_t s) {
+  ThetaParams tp{};
+  tp.N = st.N;
+  tp.A = st.tA;
+  tp.Bc = st.tBc;
+  tp.nfield = p->B * p->C;
+  tp.ncomp = p->C;
+  tp.npts = p->npts;
+  tp.W = st.tW;
+  tp.phi_class_a = st.tclass_mode;
+  tp.nclass = st.tnclass;
+  tp.phif = st.phif;
+  tp.tw = st.tw;
+  tp.X = buf_ptr(p, st.src, Wout);
+  tp.Y = buf_ptr(p, st.dst, Wout);
+  tp.Wprev = Win;
+  tp.tau = p->tau;
+  tp.limit = 1e12;
+  tp.first_bad = first_bad;
+  tp.step = p->step_dev;
+  const long long lines = (long long)tp.nfield * tp.A * tp.Bc;
+  const int span = (tp.Bc == 1) ? tp.A : tp.Bc;
+  const bool ax = st.epi == EPI_AXPY;
+  // register-resident two-phase FFT when the split M = M1*M2 exists and the
+  // lines tile the CTA; Stockham smem passes otherwise
+#define TRY_FAST(M1, M2)                                                                   \
+  if (st.N / 2 == (M1) * (M2) && span % FastTheta<M1, M2>::LPB == 0) {                     \
+    const unsigned nb = (unsigned)(lines / FastTheta<M1, M2>::LPB);                        \
+    if (ax)                                                                                \
+      theta_fast_kernel<M1, M2, true><<<nb, 256, FastTheta<M1, M2>::smem, s>>>(tp);        \
+    else                                                                                   \
+      theta_fast_kernel<M1, M2, false><<<nb, 256, FastTheta<M1, M2>::smem, s>>>(tp);       \
+    CUDA_TRY(cudaGetLastError());                                                          \
+    return CG_OK;                                                                          \
+  }
+  TRY_FAST(4, 4)
+  TRY_FAST(4, 8)
+  TRY_FAST(8, 8)
+  TRY_FAST(8, 16)
+  TRY_FAST(16, 16)
+#undef TRY_FAST
+  const unsigned blocks = (unsigned)(lines / tp.W);
+  const size_t smem = theta_smem_bytes(st.N, st.tW);
+  if (st.epi == EPI_AXPY)
+    theta_prop_kernel<true><<<blocks, 256, smem, s>>>(tp);
+  else
+    theta_prop_kernel<false><<<blocks, 256, smem, s>>>(tp);
+  CUDA_TRY(cudaGetLastError());
+  return CG_OK;
+}
+
 int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, int* first_bad, cudaStream_t s) {
   int rc;
+  if (st.var == VAR_THETA) return launch_theta(p, st, Win, Wout, first_bad, s);
   {
     const double* src = buf_ptr(p, st.src, Wout);
     double* dst = buf_ptr(p, st.dst, Wout);
@@ -433,6 +540,69 @@ int build_stages(cg_plan* p, const cg_desc* d) {
   int rc = 0;
   // phi tables
   auto up_phi = [&](const double* h, size_t per, double** out) -> int { return upload(p, h, per * C, out); };
+  const bool fft = (d->options & CG_OPT_THETA_FFT) != 0;
+  if (p->geom == CG_DISK && fft && pow2(n2)) {
+    if ((rc = need(d->phi1_rho, "phi1_rho")) || (rc = need(d->Phi, "Phi"))) return rc;
+    const double *Ph = d->Phi, *P1 = d->phi1_rho;
+    // T = Q (Phi_i o Q^T F) along theta for every rho row i, by FFT
+    if ((rc = add_theta_stage(p, EPI_STORE, BUF_X, BUF_Y, n2, n1, 1, 1, n1,
+                              [&](int c, int i, int col) { return Ph[((size_t)c * n1 + i) * n2 + col]; })))
+      return rc;
+    // W + tau * phi1_rho T
+    return add_stage(p, VAR_NN, EPI_AXPY, n1, n2, n1, 1, BUF_Y, BUF_OUT, n1,
+                     [&](int c, int r, int q) { return P1[((size_t)c * n1 + r) * n1 + q]; });
+  }
+  if (p->geom == CG_SPHERE && fft && pow2(n1)) {
+    if ((rc = need(d->phi1_phi, "phi1_phi")) || (rc = need(d->Phi, "Phi"))) return rc;
+    const double *Ph = d->Phi, *P1 = d->phi1_phi;
+    // G = F phi1_phi^T, then W + tau * Q (Phi_j o Q^T G) along theta for every column j
+    if ((rc = add_stage(p, VAR_TN, EPI_STORE, n1, n2, n2, 1, BUF_X, BUF_Y, n2,
+                        [&](int c, int r, int q) { return P1[((size_t)c * n2 + r) * n2 + q]; })))
+      return rc;
+    return add_theta_stage(p, EPI_AXPY, BUF_Y, BUF_OUT, n1, 1, n2, 0, n2,
+                           [&](int c, int j, int col) { return Ph[((size_t)c * n1 + col) * n2 + j]; });
+  }
+  if (p->geom == CG_CYLINDER && fft && pow2(n2)) {
+    if ((rc = need(d->phi1_rho, "phi1_rho")) || (rc = need(d->Phi, "Phi")) || (rc = need(d->phi1_z, "phi1_z")))
+      return rc;
+    const double *Ph = d->Phi, *Pz = d->phi1_z, *P1 = d->phi1_rho;
+    if ((rc = add_stage(p, VAR_TN, EPI_STORE, n1 * n2, n3, n3, 1, BUF_X, BUF_Y, n3,
+                        [&](int c, int r, int q) { return Pz[((size_t)c * n3 + r) * n3 + q]; })))
+      return rc;
+    if ((rc = add_theta_stage(p, EPI_STORE, BUF_Y, BUF_X, n2, n1, n3, 1, n1,
+                              [&](int c, int i, int col) { return Ph[((size_t)c * n1 + i) * n2 + col]; })))
+      return rc;
+    return add_stage(p, VAR_NN, EPI_AXPY, n1, n2 * n3, n1, 1, BUF_X, BUF_OUT, n1,
+                     [&](int c, int r, int q) { return P1[((size_t)c * n1 + r) * n1 + q]; });
+  }
+  if (p->geom == CG_BALL && fft && pow2(n2)) {
+    if ((rc = need(d->phi1_rho, "phi1_rho")) || (rc = need(d->Phi, "Phi")) ||
+        (rc = need(d->Phi_outer, "Phi_outer")) || (rc = need(d->V_phi, "V_phi")) ||
+        (rc = need(d->Vinv_phi, "Vinv_phi")))
+      return rc;
+    double* phio = nullptr;
+    if ((rc = up_phi(d->Phi_outer, (size_t)n1 * n3, &phio))) return rc;
+    const double *V = d->V_phi, *Vi = d->Vinv_phi, *P1 = d->phi1_rho, *Ph = d->Phi;
+    if ((rc = add_stage(p, VAR_TN, EPI_PHI, n1 * n2, n3, n3, 1, BUF_X, BUF_Y, n3,
+                        [&](int c, int r, int q) { return Vi[((size_t)c * n3 + r) * n3 + q]; })))
+      return rc;
+    Stage& s0 = p->stages.back();
+    s0.phi = phio;
+    s0.phi_c = (long long)n1 * n3;
+    s0.phi_rdiv = n2;
+    s0.phi_m = n3;
+    s0.phi_n = 1;
+    if ((rc = add_stage(p, VAR_TN, EPI_STORE, n1 * n2, n3, n3, 1, BUF_Y, BUF_X, n3,
+                        [&](int c, int r, int q) { return V[((size_t)c * n3 + r) * n3 + q]; })))
+      return rc;
+    if ((rc = add_theta_stage(p, EPI_STORE, BUF_X, BUF_Y, n2, n1, n3, 2, n1 * n3, [&](int c, int cls, int col) {
+           const int i = cls / n3, k = cls % n3;
+           return Ph[(((size_t)c * n1 + i) * n2 + col) * n3 + k];
+         })))
+      return rc;
+    return add_stage(p, VAR_NN, EPI_AXPY, n1, n2 * n3, n1, 1, BUF_Y, BUF_OUT, n1,
+                     [&](int c, int r, int q) { return P1[((size_t)c * n1 + r) * n1 + q]; });
+  }
   if (p->geom == CG_DISK) {
     const int nt = n2;
     if ((rc = need(Q, "Q_theta")) || (rc = need(d->phi1_rho, "phi1_rho")) || (rc = need(d->Phi, "Phi"))) return rc;
@@ -652,6 +822,25 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
     StencilParams sp{};
     if ((rc = launch_fbuild(p->geom, KIN_EXTERNAL, sp, nullptr, true))) return bail(rc);
     if ((rc = launch_fbuild(p->geom, p->kin, sp, nullptr, true))) return bail(rc);
+  }
+  {
+    cudaError_t e1 = cudaFuncSetAttribute(theta_prop_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          100 * 1024);
+    cudaError_t e2 = cudaFuncSetAttribute(theta_prop_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          100 * 1024);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
+#define OPT_IN(M1, M2)                                                                                        \
+  e1 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                            (int)FastTheta<M1, M2>::smem);                                                    \
+  e2 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                            (int)FastTheta<M1, M2>::smem);                                                    \
+  if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
+    OPT_IN(4, 4)
+    OPT_IN(4, 8)
+    OPT_IN(8, 8)
+    OPT_IN(8, 16)
+    OPT_IN(16, 16)
+#undef OPT_IN
   }
   const size_t bytes = (size_t)p->elems * sizeof(double);
   if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&p->X)))) return bail(rc);

@@ -1,0 +1,497 @@
+// Fused theta propagator: y = Q_theta diag(Phi_line) Q_theta^T x along the
+// periodic theta axis, by FFT.
+//
+// The reference applies phi1 of the theta summand as two dense mu-mode
+// products with the real Fourier eigenbasis Q_theta (operators.py:142-169)
+// around a Hadamard with a phi1 tensor (integrators.py:204-206, :211-214,
+// :232-234): T = ((X Q) o Phi) Q^T.  Because Q's columns are the
+// cos/sin pairs of frequency j with equal eigenvalues, Phi is equal on both
+// columns of a pair and the triple product is exactly
+//     y = IDFT_N( Phi_j * DFT_N(x) ),   Phi_j = Phi[col(j)],
+//     col(0) = 0, col(j) = 2j - 1 (0 < j < N/2), col(N/2) = N - 1,
+// i.e. a real circular convolution.  It is evaluated with a half-length
+// complex FFT (z_k = x_2k + i x_2k+1, M = N/2 points), the real-FFT
+// split/merge twiddles, the real Phi_j scaling, and the inverse, all in
+// shared memory: O(N log N) work instead of 2 N^2 per line, one HBM read and
+// one write per value.  N must be a power of two (radix-4 Stockham stages
+// plus at most one radix-2 stage).
+//
+// A field is viewed as [A][N][Bc] (A = axes before theta, Bc = axes after);
+// a CTA owns W lines: W consecutive a (Bc == 1, contiguous rows) or W
+// consecutive bc (Bc > 1, lines are columns).  Epilogue: store, or
+// W_out = W + tau * y with the divergence guard (sphere: theta is the last
+// factor of its chain).
+#pragma once
+
+#include "common.cuh"
+
+namespace cg {
+
+struct ThetaParams {
+  int N;             // theta extent (power of two)
+  int A, Bc;         // field = [A][N][Bc]
+  int nfield, ncomp;
+  long long npts;    // A * N * Bc
+  int W;             // lines per CTA
+  int phi_class_a;   // Phi class of a line: 1 = a (disk, cylinder), 0 = bc (sphere), 2 = a*Bc + bc (ball)
+  int nclass;        // classes per component
+  const double* phif;  // [C][nclass][N/2 + 1] Phi_j
+  const double2* tw;   // [N] exp(-2 pi i t / N)
+  const double* X;
+  double* Y;
+  const double* Wprev;  // AXPY: previous state
+  double tau, limit;
+  int* first_bad;
+  const int* step;
+};
+
+// dynamic shared memory: two [W][M+1] complex ping-pong buffers + N twiddles
+inline size_t theta_smem_bytes(int N, int W) {
+  return (size_t)(2 * W * (N / 2 + 1) + N) * sizeof(double2);
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+
+// One Stockham pass of radix R (4 or 2) over W lines of M points:
+// src/dst are [W][M + 1] (padded rows).  INV selects the inverse sign.
+template <int R, bool INV>
+__device__ __forceinline__ void stockham_pass(const double2* src, double2* dst, int M, int W, int ns,
+                                              const double2* tw, int twN) {
+  const int q = M / R;  // butterflies per line
+  const int ld = M + 1;
+  for (int idx = threadIdx.x; idx < W * q; idx += blockDim.x) {
+    const int w = idx / q;
+    const int j = idx - w * q;
+    const int k = j % ns;
+    const double2* s = src + w * ld;
+    double2* d = dst + w * ld;
+    // twiddle exp(-+2 pi i k / (R ns)) from the length-twN table
+    const int step = twN / (R * ns);
+    if (R == 4) {
+      double2 a0 = s[j], a1 = s[j + q], a2 = s[j + 2 * q], a3 = s[j + 3 * q];
+      if (ns > 1) {
+        double2 w1 = tw[k * step], w2 = tw[2 * k * step], w3 = tw[3 * k * step];
+        if (INV) {
+          w1 = cconj(w1);
+          w2 = cconj(w2);
+          w3 = cconj(w3);
+        }
+        a1 = cmul(a1, w1);
+        a2 = cmul(a2, w2);
+        a3 = cmul(a3, w3);
+      }
+      const double2 b0 = cadd(a0, a2), b1 = csub(a0, a2), b2 = cadd(a1, a3);
+      const double2 t = csub(a1, a3);
+      const double2 b3 = INV ? make_double2(-t.y, t.x) : make_double2(t.y, -t.x);  // +-i * (a1 - a3)
+      const int base = (j / ns) * 4 * ns + k;
+      d[base] = cadd(b0, b2);
+      d[base + ns] = cadd(b1, b3);
+      d[base + 2 * ns] = csub(b0, b2);
+      d[base + 3 * ns] = csub(b1, b3);
+    } else {
+      double2 a0 = s[j], a1 = s[j + q];
+      if (ns > 1) {
+        double2 w1 = tw[k * step];
+        if (INV) w1 = cconj(w1);
+        a1 = cmul(a1, w1);
+      }
+      const int base = (j / ns) * 2 * ns + k;
+      d[base] = cadd(a0, a1);
+      d[base + ns] = csub(a0, a1);
+    }
+  }
+}
+
+// Complex FFT of length M on W lines, result returned in *cur (ping-pong).
+template <bool INV>
+__device__ __forceinline__ void fft_lines(double2*& cur, double2*& alt, int M, int W, const double2* tw, int twN) {
+  int ns = 1;
+  while (ns * 4 <= M) {
+    stockham_pass<4, INV>(cur, alt, M, W, ns, tw, twN);
+    __syncthreads();
+    double2* t = cur;
+    cur = alt;
+    alt = t;
+    ns *= 4;
+  }
+  if (ns < M) {
+    stockham_pass<2, INV>(cur, alt, M, W, ns, tw, twN);
+    __syncthreads();
+    double2* t = cur;
+    cur = alt;
+    alt = t;
+  }
+}
+
+template <bool AXPY>
+__global__ void __launch_bounds__(256) theta_prop_kernel(const ThetaParams p) {
+  extern __shared__ double2 tp_smem[];
+  const int N = p.N, M = N / 2, W = p.W, ld = M + 1;
+  double2* bufA = tp_smem;
+  double2* bufB = tp_smem + W * ld;
+  double2* twS = tp_smem + 2 * W * ld;  // [N]
+
+  // CTA -> (field, a0, bc0)
+  const int Bc = p.Bc;
+  int blk = blockIdx.x;
+  int f, a0, bc0;
+  if (Bc == 1) {
+    const int per = p.A / W;
+    f = blk / per;
+    a0 = (blk - f * per) * W;
+    bc0 = 0;
+  } else {
+    const int per = Bc / W;
+    const int pa = blk / per;
+    bc0 = (blk - pa * per) * W;
+    f = pa / p.A;
+    a0 = pa - f * p.A;
+  }
+  const int c = f % p.ncomp;
+  const long long fbase = (long long)f * p.npts;
+  const long long lstride = (long long)N * Bc;  // stride between consecutive a
+
+  for (int t = threadIdx.x; t < N; t += blockDim.x) twS[t] = __ldg(p.tw + t);
+
+  // ---- load: z_k = x_2k + i x_2k+1 for each of the W lines
+  if (Bc == 1) {
+    for (int idx = threadIdx.x; idx < W * M; idx += blockDim.x) {
+      const int w = idx / M, k = idx - w * M;
+      const double2 v = __ldg(reinterpret_cast<const double2*>(p.X + fbase + (long long)(a0 + w) * lstride) + k);
+      bufA[w * ld + k] = v;
+    }
+  } else {
+    const long long base = fbase + (long long)a0 * lstride + bc0;
+    for (int idx = threadIdx.x; idx < W * M; idx += blockDim.x) {
+      const int w = idx % W, k = idx / W;
+      const double x0 = __ldg(p.X + base + (long long)(2 * k) * Bc + w);
+      const double x1 = __ldg(p.X + base + (long long)(2 * k + 1) * Bc + w);
+      bufA[w * ld + k] = make_double2(x0, x1);
+    }
+  }
+  __syncthreads();
+
+  double2* cur = bufA;
+  double2* alt = bufB;
+  fft_lines<false>(cur, alt, M, W, twS, N);
+
+  // ---- split to the real spectrum X_j (j = 0..M), scale by Phi_j, merge
+  //      back to the half-length spectrum Z'_j of the inverse (in place).
+  const int half = M / 2;
+  for (int idx = threadIdx.x; idx < W * (half + 1); idx += blockDim.x) {
+    const int w = idx / (half + 1), j = idx - w * (half + 1);
+    const int la = (Bc == 1) ? a0 + w : a0, lbc = (Bc == 1) ? 0 : bc0 + w;
+    const int cls = p.phi_class_a == 1 ? la : (p.phi_class_a == 0 ? lbc : la * Bc + lbc);
+    const double* ph = p.phif + ((long long)c * p.nclass + cls) * (M + 1);
+    double2* z = cur + w * ld;
+    if (j == 0) {
+      const double2 z0 = z[0];
+      const double x0 = (z0.x + z0.y) * ph[0];   // X_0 * Phi_0
+      const double xm = (z0.x - z0.y) * ph[M];   // X_M * Phi_M
+      // Z'_0 = (Y_0 + Y_M)/2 + i (Y_0 - Y_M)/2
+      z[0] = make_double2(0.5 * (x0 + xm), 0.5 * (x0 - xm));
+      continue;
+    }
+    const int jm = M - j;
+    const double2 zj = z[j], zm = z[jm];
+    // E_j = (Z_j + conj Z_{M-j})/2, O_j = (Z_j - conj Z_{M-j})/(2i)
+    const double2 e = make_double2(0.5 * (zj.x + zm.x), 0.5 * (zj.y - zm.y));
+    const double2 o = make_double2(0.5 * (zj.y + zm.y), -0.5 * (zj.x - zm.x));
+    const double2 wj = twS[j];  // exp(-2 pi i j / N)
+    const double2 wo = cmul(wj, o);
+    // X_j = E + w^j O,  X_{M-j} = conj(E) - conj(w^j O)  (w^{M-j} = -conj(w^j))
+    double2 xj = cadd(e, wo);
+    double2 xmj = make_double2(e.x - wo.x, -(e.y - wo.y));
+    xj.x *= ph[j];
+    xj.y *= ph[j];
+    xmj.x *= ph[jm];
+    xmj.y *= ph[jm];
+    // merge: Z'_j = (Y_j + conj Y_{M-j})/2 + i conj(w^j) (Y_j - conj Y_{M-j})/2
+    const double2 s1 = make_double2(0.5 * (xj.x + xmj.x), 0.5 * (xj.y - xmj.y));
+    const double2 d1 = make_double2(0.5 * (xj.x - xmj.x), 0.5 * (xj.y + xmj.y));
+    const double2 wd = cmul(cconj(wj), d1);
+    z[j] = make_double2(s1.x - wd.y, s1.y + wd.x);
+    if (jm != j) {
+      // Z'_{M-j} from the same pair (roles of j and M-j swapped)
+      const double2 s2 = make_double2(0.5 * (xmj.x + xj.x), 0.5 * (xmj.y - xj.y));
+      const double2 d2 = make_double2(0.5 * (xmj.x - xj.x), 0.5 * (xmj.y + xj.y));
+      const double2 wmj = make_double2(-wj.x, wj.y);  // exp(-2 pi i (M-j)/N) = -conj(w^j)
+      const double2 wd2 = cmul(cconj(wmj), d2);
+      z[jm] = make_double2(s2.x - wd2.y, s2.y + wd2.x);
+    }
+  }
+  __syncthreads();
+  fft_lines<true>(cur, alt, M, W, twS, N);
+
+  // ---- store y_2k = Re z'_k / M, y_2k+1 = Im z'_k / M (+ axpy / guard)
+  const double scale = 1.0 / (double)M;
+  bool bad = false;
+  if (Bc == 1) {
+    for (int idx = threadIdx.x; idx < W * M; idx += blockDim.x) {
+      const int w = idx / M, k = idx - w * M;
+      const double2 z = cur[w * ld + k];
+      const long long o = fbase + (long long)(a0 + w) * lstride + 2 * k;
+      double y0 = z.x * scale, y1 = z.y * scale;
+      if (AXPY) {
+        const double2 wv = __ldg(reinterpret_cast<const double2*>(p.Wprev + o));
+        y0 = __dadd_rn(wv.x, __dmul_rn(p.tau, y0));
+        y1 = __dadd_rn(wv.y, __dmul_rn(p.tau, y1));
+        bad |= !(fabs(y0) <= p.limit) || !(fabs(y1) <= p.limit);
+      }
+      *reinterpret_cast<double2*>(p.Y + o) = make_double2(y0, y1);
+    }
+  } else {
+    const long long base = fbase + (long long)a0 * lstride + bc0;
+    for (int idx = threadIdx.x; idx < W * M; idx += blockDim.x) {
+      const int w = idx % W, k = idx / W;
+      const double2 z = cur[w * ld + k];
+      const long long o0 = base + (long long)(2 * k) * Bc + w, o1 = o0 + Bc;
+      double y0 = z.x * scale, y1 = z.y * scale;
+      if (AXPY) {
+        y0 = __dadd_rn(__ldg(p.Wprev + o0), __dmul_rn(p.tau, y0));
+        y1 = __dadd_rn(__ldg(p.Wprev + o1), __dmul_rn(p.tau, y1));
+        bad |= !(fabs(y0) <= p.limit) || !(fabs(y1) <= p.limit);
+      }
+      p.Y[o0] = y0;
+      p.Y[o1] = y1;
+    }
+  }
+  if (AXPY) {
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(p.first_bad + f, *p.step);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Register-resident two-phase FFT (M = M1 * M2, M1, M2 <= 16).
+// Phase A: thread n2 takes z[n2 + M2 n1], DFT_M1 over n1 in registers,
+// twiddle w_M^(n2 k1); padded smem transpose; phase B: thread k1 takes the M2
+// values of row k1, DFT_M2 in registers -> X[k1 + M1 k2].  One smem round
+// trip per transform instead of log4(M) Stockham passes.
+// ---------------------------------------------------------------------------
+
+__host__ __device__ constexpr double cos16(int k) {
+  // cos(2 pi k / 16), exact-symmetric correctly rounded values
+  return k == 0 ? 1.0 : k == 1 ? 0.9238795325112867 : k == 2 ? 0.7071067811865476 : k == 3 ? 0.3826834323650898
+       : k == 4 ? 0.0 : k == 5 ? -0.3826834323650898 : k == 6 ? -0.7071067811865476 : k == 7 ? -0.9238795325112867
+       : k == 8 ? -1.0 : k == 9 ? -0.9238795325112867 : k == 10 ? -0.7071067811865476 : k == 11 ? -0.3826834323650898
+       : k == 12 ? 0.0 : k == 13 ? 0.3826834323650898 : k == 14 ? 0.7071067811865476 : 0.9238795325112867;
+}
+__host__ __device__ constexpr double sin16(int k) { return cos16((k + 12) & 15); }  // sin x = cos(x - pi/2)
+
+__host__ __device__ constexpr int bitrev(int i, int L) {
+  int r = 0;
+  for (int b = 1; b < L; b <<= 1) r = (r << 1) | ((i & b) ? 1 : 0);
+  return r;
+}
+
+// One radix-2 DIT stage of sub-transform length LEN, then the next (template
+// recursion so every index is a compile-time constant and `a` stays in
+// registers; nested runtime-bounded loops left it in local memory).
+template <int L, int LEN, bool INV>
+__device__ __forceinline__ void dit_stage(double2* a) {
+  constexpr int half = LEN / 2;
+#pragma unroll
+  for (int q = 0; q < L / 2; ++q) {
+    const int st = (q / half) * LEN, j = q % half;
+    const double2 u = a[st + j];
+    double2 v = a[st + j + half];
+    if (j != 0) {
+      const int t = j * (16 / LEN);
+      const double c = cos16(t), s = INV ? sin16(t) : -sin16(t);
+      v = make_double2(v.x * c - v.y * s, v.x * s + v.y * c);
+    }
+    a[st + j] = make_double2(u.x + v.x, u.y + v.y);
+    a[st + j + half] = make_double2(u.x - v.x, u.y - v.y);
+  }
+  if constexpr (LEN < L) dit_stage<L, LEN * 2, INV>(a);
+}
+
+// In-register DFT of length L (power of two <= 16), natural order in and out.
+template <int L, bool INV>
+__device__ __forceinline__ void dft_reg(double2* a) {
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    const int r = bitrev(i, L);
+    if (r > i) {
+      const double2 t = a[i];
+      a[i] = a[r];
+      a[r] = t;
+    }
+  }
+  if constexpr (L > 1) dit_stage<L, 2, INV>(a);
+}
+
+template <int M1, int M2>
+struct FastTheta {
+  static constexpr int M = M1 * M2;
+  static constexpr int TPL = M1 > M2 ? M1 : M2;  // threads per line
+  static constexpr int LPB = 256 / TPL;          // lines per CTA
+  static constexpr int LDT = M1 * (M2 + 1);      // padded transpose tile (complex)
+  static constexpr int SL0 = LDT > M ? LDT : M;
+  static constexpr int SL = (SL0 % 2 == 0) ? SL0 + 1 : SL0;  // odd line stride: lines land on distinct banks
+  static constexpr size_t smem = (size_t)LPB * SL * sizeof(double2);
+};
+
+template <int M1, int M2, bool AXPY>
+__global__ void __launch_bounds__(256) theta_fast_kernel(const ThetaParams p) {
+  using F = FastTheta<M1, M2>;
+  constexpr int M = F::M, TPL = F::TPL, LPB = F::LPB;
+  constexpr int R = TPL;
+  extern __shared__ double2 tf_smem[];
+  const int N = 2 * M;
+  const int Bc = p.Bc;
+  const int tid = threadIdx.x;
+  int ln, lt;  // line within CTA, thread within line
+  if (Bc == 1) {
+    ln = tid / TPL;
+    lt = tid - ln * TPL;
+  } else {
+    ln = tid % LPB;
+    lt = tid / LPB;
+  }
+  // CTA -> (field, a0, bc0) as in theta_prop_kernel with W = LPB
+  const int blk = blockIdx.x;
+  int f, a0, bc0;
+  if (Bc == 1) {
+    const int per = p.A / LPB;
+    f = blk / per;
+    a0 = (blk - f * per) * LPB;
+    bc0 = 0;
+  } else {
+    const int per = Bc / LPB;
+    const int pa = blk / per;
+    bc0 = (blk - pa * per) * LPB;
+    f = pa / p.A;
+    a0 = pa - f * p.A;
+  }
+  const int c = f % p.ncomp;
+  const int la = (Bc == 1) ? a0 + ln : a0, lbc = (Bc == 1) ? 0 : bc0 + ln;
+  const long long lstride = (long long)N * Bc;
+  // element t of this line: base + t * es
+  const long long base = (long long)f * p.npts + (long long)la * lstride + lbc;
+  const long long es = Bc;
+  double2* S = tf_smem + ln * F::SL;
+  const double2* tw = p.tw;
+
+  auto ldz = [&](int k) -> double2 {  // z_k = x_2k + i x_2k+1
+    if (Bc == 1) return __ldg(reinterpret_cast<const double2*>(p.X + base) + k);
+    return make_double2(__ldg(p.X + base + (2LL * k) * es), __ldg(p.X + base + (2LL * k + 1) * es));
+  };
+
+  double2 r[R];
+  // ---------------- forward phase A
+  if (lt < M2) {
+    const int n2 = lt;
+#pragma unroll
+    for (int n1 = 0; n1 < M1; ++n1) r[n1] = ldz(n2 + M2 * n1);
+    dft_reg<M1, false>(r);
+#pragma unroll
+    for (int k1 = 1; k1 < M1; ++k1) r[k1] = cmul(r[k1], __ldg(tw + 2 * n2 * k1));  // w_M^(n2 k1)
+#pragma unroll
+    for (int k1 = 0; k1 < M1; ++k1) S[k1 * (M2 + 1) + n2] = r[k1];
+  }
+  __syncthreads();
+  // ---------------- forward phase B
+  if (lt < M1) {
+#pragma unroll
+    for (int n2 = 0; n2 < M2; ++n2) r[n2] = S[lt * (M2 + 1) + n2];
+    dft_reg<M2, false>(r);
+  }
+  __syncthreads();
+  if (lt < M1) {
+#pragma unroll
+    for (int k2 = 0; k2 < M2; ++k2) S[lt + M1 * k2] = r[k2];
+  }
+  __syncthreads();
+  // ---------------- split to X_j, scale by Phi_j, merge to Z'_j (pairs j, M-j)
+  {
+    const int cls = p.phi_class_a == 1 ? la : (p.phi_class_a == 0 ? lbc : la * Bc + lbc);
+    const double* ph = p.phif + ((long long)c * p.nclass + cls) * (M + 1);
+    for (int j = lt; j <= M / 2; j += TPL) {
+      if (j == 0) {
+        const double2 z0 = S[0];
+        const double x0 = (z0.x + z0.y) * __ldg(ph);
+        const double xm = (z0.x - z0.y) * __ldg(ph + M);
+        S[0] = make_double2(0.5 * (x0 + xm), 0.5 * (x0 - xm));
+        continue;
+      }
+      const int jm = M - j;
+      const double2 zj = S[j], zm = S[jm];
+      const double2 e = make_double2(0.5 * (zj.x + zm.x), 0.5 * (zj.y - zm.y));
+      const double2 o = make_double2(0.5 * (zj.y + zm.y), -0.5 * (zj.x - zm.x));
+      const double2 wj = __ldg(tw + j);
+      const double2 wo = cmul(wj, o);
+      const double pj = __ldg(ph + j), pm = __ldg(ph + jm);
+      const double2 xj = make_double2((e.x + wo.x) * pj, (e.y + wo.y) * pj);
+      const double2 xmj = make_double2((e.x - wo.x) * pm, -(e.y - wo.y) * pm);
+      const double2 s1 = make_double2(0.5 * (xj.x + xmj.x), 0.5 * (xj.y - xmj.y));
+      const double2 d1 = make_double2(0.5 * (xj.x - xmj.x), 0.5 * (xj.y + xmj.y));
+      const double2 wd = cmul(cconj(wj), d1);
+      S[j] = make_double2(s1.x - wd.y, s1.y + wd.x);
+      if (jm != j) {
+        const double2 s2 = make_double2(0.5 * (xmj.x + xj.x), 0.5 * (xmj.y - xj.y));
+        const double2 d2 = make_double2(0.5 * (xmj.x - xj.x), 0.5 * (xmj.y + xj.y));
+        const double2 wd2 = cmul(make_double2(-wj.x, -wj.y), d2);  // conj(-conj(w^j)) = -w^j
+        S[jm] = make_double2(s2.x - wd2.y, s2.y + wd2.x);
+      }
+    }
+  }
+  __syncthreads();
+  // ---------------- inverse phase A
+  if (lt < M2) {
+    const int n2 = lt;
+#pragma unroll
+    for (int n1 = 0; n1 < M1; ++n1) r[n1] = S[n2 + M2 * n1];
+    dft_reg<M1, true>(r);
+#pragma unroll
+    for (int k1 = 1; k1 < M1; ++k1) r[k1] = cmul(r[k1], cconj(__ldg(tw + 2 * n2 * k1)));
+  }
+  __syncthreads();
+  if (lt < M2) {
+#pragma unroll
+    for (int k1 = 0; k1 < M1; ++k1) S[k1 * (M2 + 1) + lt] = r[k1];
+  }
+  __syncthreads();
+  // ---------------- inverse phase B + store (y_2k = Re z'_k / M, y_2k+1 = Im z'_k / M)
+  bool bad = false;
+  if (lt < M1) {
+#pragma unroll
+    for (int n2 = 0; n2 < M2; ++n2) r[n2] = S[lt * (M2 + 1) + n2];
+    dft_reg<M2, true>(r);
+    const double scale = 1.0 / (double)M;
+#pragma unroll
+    for (int k2 = 0; k2 < M2; ++k2) {
+      const int k = lt + M1 * k2;
+      double y0 = r[k2].x * scale, y1 = r[k2].y * scale;
+      if (Bc == 1) {
+        const long long o = base + 2LL * k;
+        if (AXPY) {
+          const double2 wv = __ldg(reinterpret_cast<const double2*>(p.Wprev + o));
+          y0 = __dadd_rn(wv.x, __dmul_rn(p.tau, y0));
+          y1 = __dadd_rn(wv.y, __dmul_rn(p.tau, y1));
+          bad |= !(fabs(y0) <= p.limit) || !(fabs(y1) <= p.limit);
+        }
+        *reinterpret_cast<double2*>(p.Y + o) = make_double2(y0, y1);
+      } else {
+        const long long o0 = base + (2LL * k) * es, o1 = o0 + es;
+        if (AXPY) {
+          y0 = __dadd_rn(__ldg(p.Wprev + o0), __dmul_rn(p.tau, y0));
+          y1 = __dadd_rn(__ldg(p.Wprev + o1), __dmul_rn(p.tau, y1));
+          bad |= !(fabs(y0) <= p.limit) || !(fabs(y1) <= p.limit);
+        }
+        p.Y[o0] = y0;
+        p.Y[o1] = y1;
+      }
+    }
+  }
+  if (AXPY) {
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(p.first_bad + f, *p.step);
+  }
+}
+
+}  // namespace cg

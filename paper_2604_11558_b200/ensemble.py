@@ -49,12 +49,12 @@ def gather_fields(local, total: int, group=None, dst: int = 0):
     return torch.cat(parts, dim=0)
 
 
-def ensemble_plan(template, kin_kind: str, params: np.ndarray, tau: float) -> SplitPlan:
+def ensemble_plan(template, kin_kind: str, params: np.ndarray, tau: float, theta: str | None = None) -> SplitPlan:
     """One batched plan: operators from the template system, per-run kinetics
     parameters ``params`` [B, P]."""
     geos = [prepare(c.ops, tau) for c in template.components]
     lifts = [float(getattr(c, "lift", 0.0)) for c in template.components]
-    return SplitPlan(geos, batch=params.shape[0], kinetics=kin_kind, kin_params=params, lifts=lifts)
+    return SplitPlan(geos, batch=params.shape[0], kinetics=kin_kind, kin_params=params, lifts=lifts, theta=theta)
 
 
 def _check_shared(systems):
@@ -98,7 +98,9 @@ class Ensemble:
     def __init__(self, template, kin_kind: str, params, tau: float):
         import torch
 
-        self.plan = ensemble_plan(template, kin_kind, np.asarray(params, dtype=np.float64), tau)
+        self.plan_template = template
+        self.plan_params = np.asarray(params, dtype=np.float64)
+        self.plan = ensemble_plan(template, kin_kind, self.plan_params, tau)
         self.tau = tau
         shape = self.plan.state_shape
         self.state = torch.empty(shape, dtype=torch.float64, device="cuda")

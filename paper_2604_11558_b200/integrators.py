@@ -185,6 +185,13 @@ def prepare(base, tau: float) -> GeometryOps:
 # plan: host operands -> libcurvigpu
 # ---------------------------------------------------------------------------
 
+import os as _os
+
+# How the periodic-theta factor Q diag(Phi) Q^T is applied: "gemm" = two dense
+# DMMA mu-mode products (the reference's formulation), "fft" = the exact
+# real-FFT propagator (csrc/thetafft.cuh).  Overridable per plan.
+THETA_MODE = _os.environ.get("CURVIGPU_THETA", "gemm")
+
 KINETICS_CODES = {
     "external": 0,
     "schnakenberg": 1,
@@ -217,7 +224,7 @@ class SplitPlan:
     """
 
     def __init__(self, geos, batch: int = 1, kinetics: str = "external",
-                 kin_params=None, lifts=None):
+                 kin_params=None, lifts=None, theta: str | None = None):
         import torch  # noqa: F401  (device memory / streams)
 
         geos = list(geos)
@@ -285,6 +292,12 @@ class SplitPlan:
             d.Phi = _native.dptr(stack(lambda o: o.phi_mix.field))
         d.kinetics = KINETICS_CODES[kinetics]
         self.kinetics = kinetics
+        theta = theta or THETA_MODE
+        if theta not in ("gemm", "fft"):
+            raise ValueError(f"theta must be 'gemm' or 'fft', got {theta!r}")
+        # 'fft' applies where n_theta is a power of two, else the plan keeps the GEMM pair
+        self.theta = theta
+        d.options = _native.CG_OPT_THETA_FFT if theta == "fft" else 0
         if kin_params is not None:
             kp = _f64(kin_params).reshape(self.batch, -1)
             keep[id(kp)] = kp
@@ -378,17 +391,18 @@ class SplitPlan:
 # reference-shaped entry points
 # ---------------------------------------------------------------------------
 
-_PLAN_CACHE: dict[int, tuple[object, SplitPlan]] = {}
+_PLAN_CACHE: dict[tuple, tuple[object, SplitPlan]] = {}
 
 
 def _plan_for(ops) -> SplitPlan:
-    hit = _PLAN_CACHE.get(id(ops))
+    key = (id(ops), THETA_MODE)
+    hit = _PLAN_CACHE.get(key)
     if hit is not None and hit[0] is ops:
         return hit[1]
     plan = SplitPlan([ops], batch=1)
     if len(_PLAN_CACHE) > 64:
         _PLAN_CACHE.clear()
-    _PLAN_CACHE[id(ops)] = (ops, plan)
+    _PLAN_CACHE[key] = (ops, plan)
     return plan
 
 

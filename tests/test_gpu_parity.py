@@ -27,6 +27,16 @@ from .conftest import rel_inf
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True, params=["gemm", "fft"])
+def theta_mode(request, monkeypatch):
+    """Every parity case runs with the theta factor as two DMMA mu-mode
+    products (the reference's formulation) and as the FFT propagator."""
+    from paper_2604_11558_b200 import integrators
+
+    monkeypatch.setattr(integrators, "THETA_MODE", request.param)
+    return request.param
+
 SMALL = {1: (16, 32), 2: (24, 16), 3: (8, 16, 16), 4: (10, 12, 10), 5: (16, 32)}
 STEP1_TOL = 1e-10
 STEP100_TOL = 1e-8
