@@ -160,7 +160,7 @@ def kernel_roofline(plan, state, reps=20):
     rows = []
     pk = peaks()
     hbm = float(pk.get("hbm_gbs", 6650.0))
-    for stage in range(-1, plan.stage_count()):
+    for stage in plan.step_kernels():
         flops, nbytes = plan.stage_info(stage)
         for _ in range(3):
             plan.run_stage(stage, state, out)
@@ -176,7 +176,7 @@ def kernel_roofline(plan, state, reps=20):
             row = {"kernel": f"gemm_stage{stage}", "bound": "tensor", "achieved": flops / sec / 1e12,
                    "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "flops_per_launch": flops}
         else:
-            name = "fbuild" if stage < 0 else f"theta_fft_stage{stage}"
+            name = {-1: "fbuild", -2: "fused_fbuild_theta_fft"}.get(stage, f"theta_fft_stage{stage}")
             row = {"kernel": name, "bound": "hbm", "achieved": nbytes / sec / 1e9, "peak": hbm,
                    "unit": "GB/s", "bytes_per_launch": nbytes}
         row["frac"] = row["achieved"] / row["peak"]

@@ -150,11 +150,16 @@ int cg_run(cg_plan* plan, double* state, long long step0, long long nsteps,
            int* first_bad, void* stream);
 
 /* Per-kernel access for measurement (bench.py roofline): stage -1 is the
- * F-build kernel (stencil + fused kinetics, reads W), stages 0..count-1 the
+ * F-build kernel (stencil + fused kinetics, reads W), stage -2 the fused disk
+ * F-build + FFT theta kernel (when the plan uses it), stages 0..count-1 the
  * GEMM chain in order; each runs on the plan's workspaces exactly as inside
  * a step (the last stage writes W_out and reads W for the axpy).  Algorithmic
  * flops per launch count 2*M*N*K per batch item over the true extents. */
 int cg_plan_stage_count(const cg_plan* plan);
+/* Kernels one cg_run step launches, in order, as stage ids (-2 = the fused
+ * disk F-build + FFT-theta kernel, -1 = F-build, >= 0 = stages); returns the
+ * count (ids beyond max_ids are not written). */
+int cg_plan_step_kernels(const cg_plan* plan, int* ids, int max_ids);
 int cg_plan_stage_info(const cg_plan* plan, int stage, long long* flops, long long* bytes);
 int cg_run_stage(cg_plan* plan, int stage, const double* W, double* W_out, int* first_bad, void* stream);
 

@@ -77,6 +77,7 @@ EXPORTS = (
     "cg_plan_stage_count",
     "cg_plan_stage_info",
     "cg_run_stage",
+    "cg_plan_step_kernels",
 )
 
 
@@ -128,6 +129,8 @@ def lib():
     L.cg_plan_stage_info.restype = ctypes.c_int
     L.cg_run_stage.argtypes = [vp, ctypes.c_int, vp, vp, vp, vp]
     L.cg_run_stage.restype = ctypes.c_int
+    L.cg_plan_step_kernels.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.c_int]
+    L.cg_plan_step_kernels.restype = ctypes.c_int
     _lib = L
     return L
 

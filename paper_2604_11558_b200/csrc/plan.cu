@@ -23,6 +23,7 @@
 #include "gemm.cuh"
 #include "stencil.cuh"
 #include "thetafft.cuh"
+#include "fused_disk.cuh"
 
 using namespace cg;
 
@@ -243,6 +244,12 @@ struct cg_plan {
   std::vector<Stage> stages;
   std::vector<GraphEntry> graphs;
   cudaStream_t cap_stream = nullptr;
+  // disk + FFT theta + built-in kinetics: F-build and stages[0] (theta) run
+  // as one fused kernel (fused_disk.cuh) inside cg_run.  Opt-in
+  // (CURVIGPU_FUSED_FRONT=1): measured slower than the two separate kernels
+  // on B200 so far (profiles/r01_v6_fused_vs_unfused.txt)
+  bool fused_front = false;
+  int fused_m1 = 0, fused_m2 = 0;
 };
 
 namespace {
@@ -521,12 +528,104 @@ int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
 }
 
 // Launch one full step: Win (+G) -> F -> stage chain -> Wout.
+template <int M1, int M2, int KIN>
+int launch_fused_t(const ThetaParams& tp, const StencilParams& sp, cudaStream_t s, bool configure_only) {
+  using D = FusedDisk<M1, M2>;
+  if (configure_only) {
+    CUDA_TRY(cudaFuncSetAttribute(disk_ftheta_kernel<M1, M2, KIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)D::smem));
+    return CG_OK;
+  }
+  const unsigned blocks = (unsigned)(sp.batch * (sp.n1 / D::RPB));
+  disk_ftheta_kernel<M1, M2, KIN><<<blocks, 256, D::smem, s>>>(tp, sp);
+  CUDA_TRY(cudaGetLastError());
+  return CG_OK;
+}
+
+template <int M1, int M2>
+int launch_fused_k(int kin, const ThetaParams& tp, const StencilParams& sp, cudaStream_t s, bool conf) {
+  switch (kin) {
+    case KIN_SCHNAKENBERG: return launch_fused_t<M1, M2, KIN_SCHNAKENBERG>(tp, sp, s, conf);
+    case KIN_BRUSSELATOR: return launch_fused_t<M1, M2, KIN_BRUSSELATOR>(tp, sp, s, conf);
+    case KIN_GRAY_SCOTT: return launch_fused_t<M1, M2, KIN_GRAY_SCOTT>(tp, sp, s, conf);
+    case KIN_BVAM_ETA: return launch_fused_t<M1, M2, KIN_BVAM_ETA>(tp, sp, s, conf);
+    case KIN_BVAM: return launch_fused_t<M1, M2, KIN_BVAM>(tp, sp, s, conf);
+    default: return launch_fused_t<M1, M2, KIN_DIB>(tp, sp, s, conf);
+  }
+}
+
+int launch_fused_front(cg_plan* p, const double* Win, bool count_step, cudaStream_t s, bool conf = false) {
+  const Stage& st = p->stages[0];
+  ThetaParams tp{};
+  tp.N = st.N;
+  tp.A = st.tA;
+  tp.Bc = 1;
+  tp.nfield = p->B * p->C;
+  tp.ncomp = p->C;
+  tp.npts = p->npts;
+  tp.phi_class_a = st.tclass_mode;
+  tp.nclass = st.tnclass;
+  tp.phif = st.phif;
+  tp.tw = st.tw;
+  tp.Y = buf_ptr(p, st.dst, nullptr);
+  StencilParams sp{};
+  sp.geometry = p->geom;
+  sp.n1 = p->n1;
+  sp.n2 = p->n2;
+  sp.n3 = p->n3;
+  sp.ncomp = p->C;
+  sp.batch = p->B;
+  sp.npts = p->npts;
+  sp.rho_b = p->rho_b;
+  sp.th = p->th;
+  sp.d_rho = p->d_rho;
+  sp.coeff = p->coeff;
+  sp.lift = p->lift;
+  sp.kin = p->kin_params;
+  sp.nparams = p->P;
+  sp.W = Win;
+  sp.step = count_step ? p->step_dev : nullptr;
+  if (p->fused_m1 == 8 && p->fused_m2 == 16) return launch_fused_k<8, 16>(p->kin, tp, sp, s, conf);
+  if (p->fused_m1 == 8 && p->fused_m2 == 8) return launch_fused_k<8, 8>(p->kin, tp, sp, s, conf);
+  if (p->fused_m1 == 16 && p->fused_m2 == 16) return launch_fused_k<16, 16>(p->kin, tp, sp, s, conf);
+  return launch_fused_k<4, 8>(p->kin, tp, sp, s, conf);
+}
+
+// Launch one full step: Win (+G) -> F -> stage chain -> Wout.
 int launch_step(cg_plan* p, const double* Win, double* Wout, const double* Gext, bool fused_kin, int* first_bad,
                 bool count_step, cudaStream_t s) {
-  int rc = launch_fstage(p, Win, Gext, fused_kin, count_step, s);
+  int rc;
+  size_t first = 0;
+  if (p->fused_front && fused_kin) {
+    if ((rc = launch_fused_front(p, Win, count_step, s))) return rc;
+    first = 1;
+  } else if ((rc = launch_fstage(p, Win, Gext, fused_kin, count_step, s))) {
+    return rc;
+  }
+  for (size_t i = first; i < p->stages.size(); ++i)
+    if ((rc = launch_stage(p, p->stages[i], Win, Wout, first_bad, s))) return rc;
+  return CG_OK;
+}
+
+// Decide whether the disk front end can run fused (after build_stages).
+int setup_fused_front(cg_plan* p) {
+  if (p->geom != CG_DISK || p->kin == CG_KIN_EXTERNAL || p->C != 2 || p->stages.empty() ||
+      p->stages[0].var != VAR_THETA || !getenv("CURVIGPU_FUSED_FRONT"))
+    return CG_OK;
+  const int M = p->n2 / 2;
+  int m1 = 0, m2 = 0;
+  if (M == 32) m1 = 4, m2 = 8;
+  if (M == 64) m1 = 8, m2 = 8;
+  if (M == 128) m1 = 8, m2 = 16;
+  if (M == 256) m1 = 16, m2 = 16;
+  if (!m1) return CG_OK;
+  const int lpb = 256 / (m1 < m2 ? m1 : m2);  // FastTheta::LPB
+  if (p->n1 % (lpb / 2) != 0) return CG_OK;
+  p->fused_m1 = m1;
+  p->fused_m2 = m2;
+  int rc = launch_fused_front(p, nullptr, false, nullptr, true);
   if (rc) return rc;
-  for (const Stage& st : p->stages)
-    if ((rc = launch_stage(p, st, Win, Wout, first_bad, s))) return rc;
+  p->fused_front = true;
   return CG_OK;
 }
 
@@ -813,6 +912,7 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
     if ((rc = bands_upload(p, d->z_bands, n_z, &p->z_b))) return bail(rc);
   }
   if ((rc = build_stages(p, d))) return bail(rc);
+  if ((rc = setup_fused_front(p))) return bail(rc);
   for (const Stage& st : p->stages) {
     CUtensorMap dummy{};
     GemmParams gp{};
@@ -862,8 +962,8 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
 int cg_plan_stage_count(const cg_plan* p) { return p ? (int)p->stages.size() : 0; }
 
 int cg_plan_stage_info(const cg_plan* p, int stage, long long* flops, long long* bytes) {
-  if (!p || stage < -1 || stage >= (int)p->stages.size()) return fail(CG_EINVAL, "bad stage index");
-  if (stage < 0) {
+  if (!p || stage < -2 || stage >= (int)p->stages.size()) return fail(CG_EINVAL, "bad stage index");
+  if (stage < 0) {  // F-build, or the fused F-build + theta kernel: read W once, write F (T) once
     if (flops) *flops = 0;
     if (bytes) *bytes = 2LL * p->elems * (long long)sizeof(double);  // read W once, write F once
     return CG_OK;
@@ -875,10 +975,30 @@ int cg_plan_stage_info(const cg_plan* p, int stage, long long* flops, long long*
   return CG_OK;
 }
 
+int cg_plan_step_kernels(const cg_plan* p, int* ids, int max_ids) {
+  if (!p || !ids) return fail(CG_EINVAL, "null argument");
+  int n = 0;
+  auto push = [&](int v) {
+    if (n < max_ids) ids[n] = v;
+    ++n;
+  };
+  size_t first = 0;
+  if (p->fused_front && p->kin != CG_KIN_EXTERNAL) {
+    push(-2);
+    first = 1;
+  } else {
+    push(-1);
+  }
+  for (size_t i = first; i < p->stages.size(); ++i) push((int)i);
+  return n;
+}
+
 int cg_run_stage(cg_plan* p, int stage, const double* W, double* W_out, int* first_bad, void* stream) {
   if (!p || !W || !W_out) return fail(CG_EINVAL, "null argument");
-  if (stage < -1 || stage >= (int)p->stages.size()) return fail(CG_EINVAL, "bad stage index");
+  if (stage < -2 || stage >= (int)p->stages.size()) return fail(CG_EINVAL, "bad stage index");
+  if (stage == -2 && !p->fused_front) return fail(CG_EINVAL, "plan has no fused front kernel");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (stage == -2) return launch_fused_front(p, W, false, s);
   if (stage < 0) return launch_fstage(p, W, nullptr, p->kin != CG_KIN_EXTERNAL, false, s);
   return launch_stage(p, p->stages[stage], W, W_out, first_bad ? first_bad : p->scratch_bad, s);
 }

@@ -329,7 +329,9 @@ __device__ __forceinline__ void dft_reg(double2* a) {
 template <int M1, int M2>
 struct FastTheta {
   static constexpr int M = M1 * M2;
-  static constexpr int TPL = M1 > M2 ? M1 : M2;  // threads per line
+  // threads per line = min(M1, M2): in each phase every thread runs
+  // max/min DFTs, so no lane idles during the heavy phase
+  static constexpr int TPL = M1 < M2 ? M1 : M2;
   static constexpr int LPB = 256 / TPL;          // lines per CTA
   static constexpr int LDT = M1 * (M2 + 1);      // padded transpose tile (complex)
   static constexpr int SL0 = LDT > M ? LDT : M;
@@ -337,75 +339,46 @@ struct FastTheta {
   static constexpr size_t smem = (size_t)LPB * SL * sizeof(double2);
 };
 
+// forward phase A for column n2: M1 loaded values -> DFT_M1 -> twiddle -> S
+template <int M1, int M2, bool INV>
+__device__ __forceinline__ void phase_a(double2* r, double2* S, int n2, const double2* tw) {
+  dft_reg<M1, INV>(r);
+#pragma unroll
+  for (int k1 = 1; k1 < M1; ++k1) {
+    const double2 w = __ldg(tw + 2 * n2 * k1);  // w_M^(n2 k1) from the length-2M table
+    r[k1] = cmul(r[k1], INV ? cconj(w) : w);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < M1; ++k1) S[k1 * (M2 + 1) + n2] = r[k1];
+}
+
+// Everything after forward phase A (every column's M1 twiddled values are in
+// S's padded transpose layout, not yet synchronised): forward phase B, real
+// split, Phi, merge, inverse FFT, scaled store (+ W + tau*y and the guard).
 template <int M1, int M2, bool AXPY>
-__global__ void __launch_bounds__(256) theta_fast_kernel(const ThetaParams p) {
+__device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int lt, int la, int lbc, int c, int f,
+                                           long long base, long long es, int Bc) {
   using F = FastTheta<M1, M2>;
-  constexpr int M = F::M, TPL = F::TPL, LPB = F::LPB;
-  constexpr int R = TPL;
-  extern __shared__ double2 tf_smem[];
-  const int N = 2 * M;
-  const int Bc = p.Bc;
-  const int tid = threadIdx.x;
-  int ln, lt;  // line within CTA, thread within line
-  if (Bc == 1) {
-    ln = tid / TPL;
-    lt = tid - ln * TPL;
-  } else {
-    ln = tid % LPB;
-    lt = tid / LPB;
-  }
-  // CTA -> (field, a0, bc0) as in theta_prop_kernel with W = LPB
-  const int blk = blockIdx.x;
-  int f, a0, bc0;
-  if (Bc == 1) {
-    const int per = p.A / LPB;
-    f = blk / per;
-    a0 = (blk - f * per) * LPB;
-    bc0 = 0;
-  } else {
-    const int per = Bc / LPB;
-    const int pa = blk / per;
-    bc0 = (blk - pa * per) * LPB;
-    f = pa / p.A;
-    a0 = pa - f * p.A;
-  }
-  const int c = f % p.ncomp;
-  const int la = (Bc == 1) ? a0 + ln : a0, lbc = (Bc == 1) ? 0 : bc0 + ln;
-  const long long lstride = (long long)N * Bc;
-  // element t of this line: base + t * es
-  const long long base = (long long)f * p.npts + (long long)la * lstride + lbc;
-  const long long es = Bc;
-  double2* S = tf_smem + ln * F::SL;
+  constexpr int M = F::M, TPL = F::TPL;
+  constexpr int RMAX = M1 > M2 ? M1 : M2;
+  double2 r[RMAX];
   const double2* tw = p.tw;
-
-  auto ldz = [&](int k) -> double2 {  // z_k = x_2k + i x_2k+1
-    if (Bc == 1) return __ldg(reinterpret_cast<const double2*>(p.X + base) + k);
-    return make_double2(__ldg(p.X + base + (2LL * k) * es), __ldg(p.X + base + (2LL * k + 1) * es));
-  };
-
-  double2 r[R];
-  // ---------------- forward phase A
-  if (lt < M2) {
-    const int n2 = lt;
+  __syncthreads();
+  // ---------------- forward phase B: rows k1 = lt, lt + TPL, ...
+  double2 keep[M1 / TPL][M2];
 #pragma unroll
-    for (int n1 = 0; n1 < M1; ++n1) r[n1] = ldz(n2 + M2 * n1);
-    dft_reg<M1, false>(r);
+  for (int q = 0; q < M1 / TPL; ++q) {
+    const int k1 = lt + q * TPL;
 #pragma unroll
-    for (int k1 = 1; k1 < M1; ++k1) r[k1] = cmul(r[k1], __ldg(tw + 2 * n2 * k1));  // w_M^(n2 k1)
-#pragma unroll
-    for (int k1 = 0; k1 < M1; ++k1) S[k1 * (M2 + 1) + n2] = r[k1];
+    for (int n2 = 0; n2 < M2; ++n2) keep[q][n2] = S[k1 * (M2 + 1) + n2];
+    dft_reg<M2, false>(keep[q]);
   }
   __syncthreads();
-  // ---------------- forward phase B
-  if (lt < M1) {
 #pragma unroll
-    for (int n2 = 0; n2 < M2; ++n2) r[n2] = S[lt * (M2 + 1) + n2];
-    dft_reg<M2, false>(r);
-  }
-  __syncthreads();
-  if (lt < M1) {
+  for (int q = 0; q < M1 / TPL; ++q) {
+    const int k1 = lt + q * TPL;
 #pragma unroll
-    for (int k2 = 0; k2 < M2; ++k2) S[lt + M1 * k2] = r[k2];
+    for (int k2 = 0; k2 < M2; ++k2) S[k1 + M1 * k2] = keep[q][k2];
   }
   __syncthreads();
   // ---------------- split to X_j, scale by Phi_j, merge to Z'_j (pairs j, M-j)
@@ -442,31 +415,30 @@ __global__ void __launch_bounds__(256) theta_fast_kernel(const ThetaParams p) {
     }
   }
   __syncthreads();
-  // ---------------- inverse phase A
-  if (lt < M2) {
-    const int n2 = lt;
+  // ---------------- inverse phase A: columns n2 = lt, lt + TPL, ...
+  double2 keepa[M2 / TPL][M1];
 #pragma unroll
-    for (int n1 = 0; n1 < M1; ++n1) r[n1] = S[n2 + M2 * n1];
-    dft_reg<M1, true>(r);
+  for (int q = 0; q < M2 / TPL; ++q) {
+    const int n2 = lt + q * TPL;
 #pragma unroll
-    for (int k1 = 1; k1 < M1; ++k1) r[k1] = cmul(r[k1], cconj(__ldg(tw + 2 * n2 * k1)));
+    for (int n1 = 0; n1 < M1; ++n1) keepa[q][n1] = S[n2 + M2 * n1];
   }
   __syncthreads();
-  if (lt < M2) {
 #pragma unroll
-    for (int k1 = 0; k1 < M1; ++k1) S[k1 * (M2 + 1) + lt] = r[k1];
-  }
+  for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, true>(keepa[q], S, lt + q * TPL, tw);
   __syncthreads();
   // ---------------- inverse phase B + store (y_2k = Re z'_k / M, y_2k+1 = Im z'_k / M)
   bool bad = false;
-  if (lt < M1) {
+  const double scale = 1.0 / (double)M;
 #pragma unroll
-    for (int n2 = 0; n2 < M2; ++n2) r[n2] = S[lt * (M2 + 1) + n2];
+  for (int q = 0; q < M1 / TPL; ++q) {
+    const int k1 = lt + q * TPL;
+#pragma unroll
+    for (int n2 = 0; n2 < M2; ++n2) r[n2] = S[k1 * (M2 + 1) + n2];
     dft_reg<M2, true>(r);
-    const double scale = 1.0 / (double)M;
 #pragma unroll
     for (int k2 = 0; k2 < M2; ++k2) {
-      const int k = lt + M1 * k2;
+      const int k = k1 + M1 * k2;
       double y0 = r[k2].x * scale, y1 = r[k2].y * scale;
       if (Bc == 1) {
         const long long o = base + 2LL * k;
@@ -492,6 +464,63 @@ __global__ void __launch_bounds__(256) theta_fast_kernel(const ThetaParams p) {
   if (AXPY) {
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(p.first_bad + f, *p.step);
   }
+}
+
+template <int M1, int M2, bool AXPY>
+__global__ void __launch_bounds__(256) theta_fast_kernel(const ThetaParams p) {
+  using F = FastTheta<M1, M2>;
+  constexpr int M = F::M, TPL = F::TPL, LPB = F::LPB;
+  extern __shared__ double2 tf_smem[];
+  const int N = 2 * M;
+  const int Bc = p.Bc;
+  const int tid = threadIdx.x;
+  int ln, lt;  // line within CTA, thread within line
+  if (Bc == 1) {
+    ln = tid / TPL;
+    lt = tid - ln * TPL;
+  } else {
+    ln = tid % LPB;
+    lt = tid / LPB;
+  }
+  // CTA -> (field, a0, bc0) with W = LPB lines
+  const int blk = blockIdx.x;
+  int f, a0, bc0;
+  if (Bc == 1) {
+    const int per = p.A / LPB;
+    f = blk / per;
+    a0 = (blk - f * per) * LPB;
+    bc0 = 0;
+  } else {
+    const int per = Bc / LPB;
+    const int pa = blk / per;
+    bc0 = (blk - pa * per) * LPB;
+    f = pa / p.A;
+    a0 = pa - f * p.A;
+  }
+  const int c = f % p.ncomp;
+  const int la = (Bc == 1) ? a0 + ln : a0, lbc = (Bc == 1) ? 0 : bc0 + ln;
+  const long long lstride = (long long)N * Bc;
+  const long long base = (long long)f * p.npts + (long long)la * lstride + lbc;  // element t at base + t*es
+  const long long es = Bc;
+  double2* S = tf_smem + ln * F::SL;
+
+  // forward phase A: columns n2 = lt, lt + TPL, ...; z_k = x_2k + i x_2k+1
+  double2 keepa[M2 / TPL][M1];
+#pragma unroll
+  for (int q = 0; q < M2 / TPL; ++q) {
+    const int n2 = lt + q * TPL;
+#pragma unroll
+    for (int n1 = 0; n1 < M1; ++n1) {
+      const int k = n2 + M2 * n1;
+      if (Bc == 1)
+        keepa[q][n1] = __ldg(reinterpret_cast<const double2*>(p.X + base) + k);
+      else
+        keepa[q][n1] = make_double2(__ldg(p.X + base + (2LL * k) * es), __ldg(p.X + base + (2LL * k + 1) * es));
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, false>(keepa[q], S, lt + q * TPL, p.tw);
+  theta_tail<M1, M2, AXPY>(p, S, lt, la, lbc, c, f, base, es, Bc);
 }
 
 }  // namespace cg

@@ -369,6 +369,14 @@ class SplitPlan:
                       "cg_plan_stage_info")
         return int(fl.value), int(by.value)
 
+    def step_kernels(self) -> list[int]:
+        """Stage ids one cg_run step launches (-2 fused front, -1 F-build)."""
+        ids = (ctypes.c_int * 32)()
+        n = self._lib.cg_plan_step_kernels(self._h, ids, 32)
+        if n < 0:
+            _native.check(n, "cg_plan_step_kernels")
+        return [ids[i] for i in range(min(n, 32))]
+
     def run_stage(self, stage: int, W, out):
         self._check_state(W, "W")
         self._check_state(out, "out")
