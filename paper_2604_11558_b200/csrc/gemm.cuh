@@ -53,31 +53,41 @@ struct StageBytes {
   static constexpr int A = BM * 128;  // BM x 16 doubles (TN) == BM/16 boxes of 16x16 (NN)
   static constexpr int B = BN * 128;
   static constexpr int total = A + B;
+  static constexpr int epi = BM * BN * 8;  // epilogue tile: W in (axpy) / result out
 };
 
 template <int BM, int BN, int STAGES>
 constexpr int gemm_smem_bytes() {
-  return STAGES * StageBytes<BM, BN>::total + 2 * STAGES * 8 + 1024;
+  return STAGES * StageBytes<BM, BN>::total + StageBytes<BM, BN>::epi + (2 * STAGES + 2) * 8 + 1024;
 }
 
 // Row permutation within an 8-row group used by the TN fragments: rows of a
 // half-warp land on distinct 128B-swizzle phases.
 __device__ __forceinline__ int perm8(int g) { return ((g & 3) << 1) | (g >> 2); }
 
+// mapA / mapB: operand tensor maps (128B swizzle).  mapW: previous state,
+// mapO: output, both viewed as (N, M, slab, field) with a (BN, BM) box; the
+// epilogue tile goes through shared memory: W arrives by TMA during the
+// mainloop, results leave by a bulk tensor store.
 template <int VAR, int BM, int BN, int WM, int WN, int STAGES, int EPI, int MINB>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
     gemm_f64_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                    const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapO,
                     const GemmParams p) {
   constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   constexpr int NCW = WARPS_M * WARPS_N;  // consumer warps
   constexpr int MT = WM / 8, NT = WN / 8;
   constexpr int SA = StageBytes<BM, BN>::A, SB = StageBytes<BM, BN>::B;
   constexpr int STAGE = SA + SB;
+  constexpr int EPIB = StageBytes<BM, BN>::epi;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  double* etile = reinterpret_cast<double*>(smem + STAGES * STAGE);  // [BM][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE + EPIB);
   uint64_t* empty = full + STAGES;
+  uint64_t* epi_full = empty + STAGES;   // W tile landed (axpy)
+  uint64_t* epi_empty = epi_full + 1;    // previous tile's store has read etile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KT = (p.K + 15) >> 4;
@@ -88,6 +98,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], NCW);
     }
+    mbar_init(epi_full, 1);
+    mbar_init(epi_empty, 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -102,8 +114,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
     if (lane == 0) {
       tma_prefetch_desc(&mapA);
       tma_prefetch_desc(&mapB);
-      int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      int it = 0, tc = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tc) {
         int r = tile;
         const int tn = r % p.tiles_n;
         r /= p.tiles_n;
@@ -128,6 +140,12 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
             for (int q = 0; q < BN / 16; ++q) tma_load_4d(sb + q * 2048, &mapB, &full[st], n0 + 16 * q, kt * 16, s, f);
           }
         }
+        if (EPI == EPI_AXPY) {
+          // W tile for this tile's epilogue, once the previous tile's store has drained etile
+          if (tc > 0) mbar_wait(epi_empty, (tc - 1) & 1);
+          mbar_arrive_expect_tx(epi_full, EPIB);
+          tma_load_4d(etile, &mapW, epi_full, n0, m0, s, f);
+        }
       }
     }
     return;
@@ -139,9 +157,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
   const int g = lane >> 2, tq = lane & 3;
   int step_now = 0;
   if (EPI == EPI_AXPY) step_now = *p.step;
-  int it = 0;
+  int it = 0, tc = 0;
 
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tc) {
     int r = tile;
     const int tn = r % p.tiles_n;
     r /= p.tiles_n;
@@ -209,7 +227,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
       if (lane == 0) mbar_arrive(&empty[st]);
     }
 
-    // ---------------- fused epilogue ----------------
+    // ---------------- fused epilogue through the shared-memory tile ----------------
     int col_in8;
     if (VAR == VAR_TN) {
       // thread holds cols perm8(2t), perm8(2t+1) = {0,2},{4,6},{1,3},{5,7};
@@ -232,64 +250,67 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
     }
     const int row_in8 = (VAR == VAR_TN) ? perm8(g) : g;
 
-    const long long base = (long long)f * p.out_f + (long long)s * p.out_s;
+    if (EPI == EPI_AXPY)
+      mbar_wait(epi_full, tc & 1);  // W tile is in etile
+    else if (tc > 0)
+      mbar_wait(epi_empty, (tc - 1) & 1);  // previous tile's store has read etile
     bool bad = false;
-    // Gather the epilogue operands (W pair or two phi1 values per accumulator
-    // pair) for a group of EC fragment rows with all loads in flight at once,
-    // then combine and store: load latency is paid once per group instead of
-    // once per fragment.  EC < MT bounds the registers at 2+ CTAs per SM.
+    // Phi1 operands for EPI_PHI (L2-resident table), all loads in flight per row group
     constexpr int EC = (MINB >= 2 && MT > 2) ? MT / 2 : MT;
 #pragma unroll
     for (int i0 = 0; i0 < MT; i0 += EC) {
-      double2 opnd[EC][NT];
-      if (EPI != EPI_STORE) {
+      double2 ph[EC][NT];
+      if (EPI == EPI_PHI) {
 #pragma unroll
         for (int ii = 0; ii < EC; ++ii) {
           int m = m0 + wm0 + (i0 + ii) * 8 + row_in8;
           if (m >= p.M) m = 0;
-          const double* phirow = nullptr;
-          if (EPI == EPI_PHI) phirow = p.phi + c * p.phi_c + s * p.phi_s + (long long)(m / p.phi_rdiv) * p.phi_m;
+          const double* phirow = p.phi + c * p.phi_c + s * p.phi_s + (long long)(m / p.phi_rdiv) * p.phi_m;
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             int n = n0 + wn0 + j * 8 + col_in8;
             if (n >= p.N) n = 0;
-            if (EPI == EPI_PHI) {
-              opnd[ii][j].x = __ldg(phirow + (long long)n * p.phi_n);
-              opnd[ii][j].y = __ldg(phirow + (long long)(n + 1) * p.phi_n);
-            } else {
-              opnd[ii][j] = __ldg(reinterpret_cast<const double2*>(p.w + base + (long long)m * p.ldc + n));
-            }
+            ph[ii][j].x = __ldg(phirow + (long long)n * p.phi_n);
+            ph[ii][j].y = __ldg(phirow + (long long)(n + 1) * p.phi_n);
           }
         }
       }
 #pragma unroll
       for (int ii = 0; ii < EC; ++ii) {
         const int i = i0 + ii;
-        const int m = m0 + wm0 + i * 8 + row_in8;
-        if (m >= p.M) continue;
+        const int ml = wm0 + i * 8 + row_in8;
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
-          const int n = n0 + wn0 + j * 8 + col_in8;
-          if (n >= p.N) continue;
-          const long long idx = base + (long long)m * p.ldc + n;
+          const int nl = wn0 + j * 8 + col_in8;
+          double2* slot = reinterpret_cast<double2*>(etile + ml * BN + nl);
           double v0 = acc[i][j][0], v1 = acc[i][j][1];
           if (EPI == EPI_PHI) {
-            v0 *= opnd[ii][j].x;
-            v1 *= opnd[ii][j].y;
+            v0 *= ph[ii][j].x;
+            v1 *= ph[ii][j].y;
           } else if (EPI == EPI_AXPY) {
+            const double2 w2 = *slot;
             // W + tau*T rounded as the reference rounds it (no FMA contraction)
-            v0 = __dadd_rn(opnd[ii][j].x, __dmul_rn(p.tau, v0));
-            v1 = __dadd_rn(opnd[ii][j].y, __dmul_rn(p.tau, v1));
-            bad |= !(fabs(v0) <= p.limit) || !(fabs(v1) <= p.limit);
+            v0 = __dadd_rn(w2.x, __dmul_rn(p.tau, v0));
+            v1 = __dadd_rn(w2.y, __dmul_rn(p.tau, v1));
+            bad |= !(fabs(v0) <= p.limit) || !(fabs(v1) <= p.limit);  // OOB entries are 0
           }
-          *reinterpret_cast<double2*>(p.out + idx) = make_double2(v0, v1);
+          *slot = make_double2(v0, v1);
         }
       }
+    }
+    fence_proxy_async_smem();
+    named_bar(1, NCW * 32);
+    if (threadIdx.x == 0) {
+      tma_store_4d(&mapO, etile, n0, m0, s, f);  // clipped to the tensor bounds
+      bulk_commit();
+      bulk_wait_read0();
+      mbar_arrive(epi_empty);
     }
     if (EPI == EPI_AXPY) {
       if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(p.first_bad + f, step_now);
     }
   }
+  if (threadIdx.x == 0) bulk_wait0();
 }
 
 }  // namespace cg

@@ -62,7 +62,7 @@ EncodeTiledFn encode_fn() {
 
 // fp64 tensor map, 128B swizzle, zero fill; dims innermost first, strides in bytes.
 int make_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-             const uint32_t* box) {
+             const uint32_t* box, bool swizzle = true) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(CG_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t gd[5], gs[4];
@@ -74,7 +74,8 @@ int make_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
   }
   for (int i = 0; i < rank - 1; ++i) gs[i] = strides_bytes[i];
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), gd, gs, bx, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(CG_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return CG_OK;
@@ -104,8 +105,8 @@ constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {
 // configure_only: set the dynamic shared memory opt-in (done at plan
 // creation, never inside a stream capture).
 template <int VAR, int BM, int BN, int WM, int WN, int ST, int MINB, int EPI>
-int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams& p, cudaStream_t stream,
-                  bool configure_only) {
+int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mw, const CUtensorMap& mo,
+                  const GemmParams& p, cudaStream_t stream, bool configure_only) {
   auto kern = gemm_f64_kernel<VAR, BM, BN, WM, WN, ST, EPI, MINB>;
   constexpr int smem = gemm_smem_bytes<BM, BN, ST>();
   constexpr int threads = (BM / WM) * (BN / WN) * 32 + 32;
@@ -124,35 +125,37 @@ int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams
   if (tiles > INT_MAX) return fail(CG_EUNSUPPORTED, "grid too large");
   // persistent grid: at most one wave of resident CTAs, each looping over tiles
   const long long blocks = (resident > 0 && tiles > resident) ? resident : tiles;
-  kern<<<(unsigned)blocks, threads, smem, stream>>>(ma, mb, p);
+  kern<<<(unsigned)blocks, threads, smem, stream>>>(ma, mb, mw, mo, p);
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
 }
 
+struct Maps {
+  CUtensorMap a, b, w, o;
+};
+
 template <int VAR, int EPI>
-int launch_gemm_cfg(int cfg, const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams& p,
-                    cudaStream_t stream, bool conf) {
+int launch_gemm_cfg(int cfg, const Maps& m, const GemmParams& p, cudaStream_t stream, bool conf) {
   switch (cfg) {
-    case 0: return launch_gemm_t<VAR, CFG0, EPI>(ma, mb, p, stream, conf);
-    case 1: return launch_gemm_t<VAR, CFG1, EPI>(ma, mb, p, stream, conf);
-    case 2: return launch_gemm_t<VAR, CFG2, EPI>(ma, mb, p, stream, conf);
-    case 3: return launch_gemm_t<VAR, CFG3, EPI>(ma, mb, p, stream, conf);
-    case 4: return launch_gemm_t<VAR, CFG4, EPI>(ma, mb, p, stream, conf);
-    case 5: return launch_gemm_t<VAR, CFG5, EPI>(ma, mb, p, stream, conf);
-    default: return launch_gemm_t<VAR, CFG6, EPI>(ma, mb, p, stream, conf);
+    case 0: return launch_gemm_t<VAR, CFG0, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case 1: return launch_gemm_t<VAR, CFG1, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case 2: return launch_gemm_t<VAR, CFG2, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case 3: return launch_gemm_t<VAR, CFG3, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case 4: return launch_gemm_t<VAR, CFG4, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case 5: return launch_gemm_t<VAR, CFG5, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
+    default: return launch_gemm_t<VAR, CFG6, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
   }
 }
 
-int launch_gemm(int var, int epi, int cfg, const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams& p,
-                cudaStream_t s, bool conf = false) {
+int launch_gemm(int var, int epi, int cfg, const Maps& m, const GemmParams& p, cudaStream_t s, bool conf = false) {
   if (var == VAR_TN) {
-    if (epi == EPI_STORE) return launch_gemm_cfg<VAR_TN, EPI_STORE>(cfg, ma, mb, p, s, conf);
-    if (epi == EPI_PHI) return launch_gemm_cfg<VAR_TN, EPI_PHI>(cfg, ma, mb, p, s, conf);
-    return launch_gemm_cfg<VAR_TN, EPI_AXPY>(cfg, ma, mb, p, s, conf);
+    if (epi == EPI_STORE) return launch_gemm_cfg<VAR_TN, EPI_STORE>(cfg, m, p, s, conf);
+    if (epi == EPI_PHI) return launch_gemm_cfg<VAR_TN, EPI_PHI>(cfg, m, p, s, conf);
+    return launch_gemm_cfg<VAR_TN, EPI_AXPY>(cfg, m, p, s, conf);
   }
-  if (epi == EPI_STORE) return launch_gemm_cfg<VAR_NN, EPI_STORE>(cfg, ma, mb, p, s, conf);
-  if (epi == EPI_PHI) return launch_gemm_cfg<VAR_NN, EPI_PHI>(cfg, ma, mb, p, s, conf);
-  return launch_gemm_cfg<VAR_NN, EPI_AXPY>(cfg, ma, mb, p, s, conf);
+  if (epi == EPI_STORE) return launch_gemm_cfg<VAR_NN, EPI_STORE>(cfg, m, p, s, conf);
+  if (epi == EPI_PHI) return launch_gemm_cfg<VAR_NN, EPI_PHI>(cfg, m, p, s, conf);
+  return launch_gemm_cfg<VAR_NN, EPI_AXPY>(cfg, m, p, s, conf);
 }
 
 __global__ void set_step_kernel(int* step, int value) { *step = value; }
@@ -307,16 +310,15 @@ int pick_cfg(int var, long long nbatch, int M, int N, int stage_index) {
     const int v = nv == 1 ? vals[0] : (stage_index < nv ? vals[stage_index] : -1);
     if (v >= 0 && v < kNumCfg) return v;
   }
-  // Measured on B200 (tools/sweep_tiles.py, profiles/r01_tile_sweep.txt):
-  // NN stages are best with 64x64 tiles, 2 CTAs/SM; TN stages with 64x128
-  // tiles at 2 CTAs/SM when N is a multiple of 128 and there are >= 2 waves,
-  // else 64x64 with a 6-deep ring at 3 CTAs/SM.
-  auto ctas = [&](int c) {
-    return nbatch * ((M + kCfgs[c].BM - 1) / kCfgs[c].BM) * ((N + kCfgs[c].BN - 1) / kCfgs[c].BN);
-  };
-  if (var == VAR_NN) return 2;
-  if (N % 128 == 0 && ctas(4) >= 2 * 148) return 4;
-  return 6;
+  // Measured on B200 with the TMA epilogue (tools/sweep_tiles.py,
+  // profiles/r01_tile_sweep_tmaepi.txt): 64x64 tiles, 4-stage ring, 2 CTAs/SM
+  // is the best or within 2% of the best for every stage of every BASELINE
+  // config (larger epilogue tiles cost occupancy).
+  (void)var;
+  (void)nbatch;
+  (void)M;
+  (void)N;
+  return 2;
 }
 
 // Build one GEMM stage: operator L (n x n) via `get`, shapes, epilogue.
@@ -518,11 +520,23 @@ int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
     gp.limit = 1e12;  // DIVERGENCE_LIMIT, integrators.py:33
     gp.first_bad = first_bad;
     gp.step = p->step_dev;
-    if (st.var == VAR_TN)
-      rc = launch_gemm(st.var, st.epi, st.cfg, smap, st.opmap, gp, s);
-    else
-      rc = launch_gemm(st.var, st.epi, st.cfg, st.opmap, smap, gp, s);
-    if (rc) return rc;
+    Maps mp;
+    mp.a = (st.var == VAR_TN) ? smap : st.opmap;
+    mp.b = (st.var == VAR_TN) ? st.opmap : smap;
+    {
+      // output (and, for the axpy epilogue, the previous state) as (N, M, slab, field), (BN, BM) boxes
+      const uint64_t dims[4] = {(uint64_t)st.N, (uint64_t)st.M, (uint64_t)st.nslab, (uint64_t)nfield};
+      const uint64_t slab = st.nslab > 1 ? (uint64_t)gp.out_s : (uint64_t)st.M * st.N;
+      const uint64_t strides[3] = {(uint64_t)st.N * 8, slab * 8, (uint64_t)p->npts * 8};
+      const uint32_t box[4] = {(uint32_t)tc.BN, (uint32_t)tc.BM, 1, 1};
+      if ((rc = make_map(&mp.o, dst, 4, dims, strides, box, false))) return rc;
+      if (st.epi == EPI_AXPY) {
+        if ((rc = make_map(&mp.w, Win, 4, dims, strides, box, false))) return rc;
+      } else {
+        mp.w = mp.o;
+      }
+    }
+    if ((rc = launch_gemm(st.var, st.epi, st.cfg, mp, gp, s))) return rc;
   }
   return CG_OK;
 }
@@ -914,9 +928,10 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
   if ((rc = build_stages(p, d))) return bail(rc);
   if ((rc = setup_fused_front(p))) return bail(rc);
   for (const Stage& st : p->stages) {
-    CUtensorMap dummy{};
+    if (st.var == VAR_THETA) continue;
+    Maps dummy{};
     GemmParams gp{};
-    if ((rc = launch_gemm(st.var, st.epi, st.cfg, dummy, dummy, gp, nullptr, true))) return bail(rc);
+    if ((rc = launch_gemm(st.var, st.epi, st.cfg, dummy, gp, nullptr, true))) return bail(rc);
   }
   {
     StencilParams sp{};
