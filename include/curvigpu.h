@@ -162,6 +162,8 @@ int cg_plan_stage_count(const cg_plan* plan);
 int cg_plan_step_kernels(const cg_plan* plan, int* ids, int max_ids);
 int cg_plan_stage_info(const cg_plan* plan, int stage, long long* flops, long long* bytes);
 int cg_run_stage(cg_plan* plan, int stage, const double* W, double* W_out, int* first_bad, void* stream);
+/* Copy a plan workspace (0 = X, 1 = Y, 2 = second state) to dst (debugging / tests). */
+int cg_plan_copy_workspace(cg_plan* plan, int which, double* dst, void* stream);
 
 /* Last error message of the calling thread. */
 const char* cg_last_error(void);

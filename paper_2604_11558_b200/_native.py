@@ -78,6 +78,7 @@ EXPORTS = (
     "cg_plan_stage_info",
     "cg_run_stage",
     "cg_plan_step_kernels",
+    "cg_plan_copy_workspace",
 )
 
 
@@ -131,6 +132,8 @@ def lib():
     L.cg_run_stage.restype = ctypes.c_int
     L.cg_plan_step_kernels.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.c_int]
     L.cg_plan_step_kernels.restype = ctypes.c_int
+    L.cg_plan_copy_workspace.argtypes = [vp, ctypes.c_int, vp, vp]
+    L.cg_plan_copy_workspace.restype = ctypes.c_int
     _lib = L
     return L
 

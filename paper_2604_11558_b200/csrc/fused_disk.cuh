@@ -63,13 +63,22 @@ __global__ void __launch_bounds__(256) disk_ftheta_kernel(const ThetaParams tp, 
   const double* Wu = Wst;
   const double* Wv = Wst + (RPB + 2) * N;
 
+  const CompCoef kc = comp_coef<0>(sp, comp, 0, N);
+  RowCoef rc;
+  {
+    const double* bands = sp.rho_b + (long long)comp * 3 * n1;
+    rc.a = bands[row];
+    rc.b = (row < n1 - 1) ? bands[n1 + row] : 0.0;
+    rc.c = (row > 0) ? bands[2 * n1 + row - 1] : 0.0;
+    rc.d = sp.d_rho[comp * n1 + row];
+  }
   auto fval = [&](int t) -> double {
     double u = Wu[(rr + 1) * N + t], v = Wv[(rr + 1) * N + t];
     if (sp.lift[0] != 0.0) u = __dadd_rn(u, sp.lift[0]);
     if (sp.lift[1] != 0.0) v = __dadd_rn(v, sp.lift[1]);
     double g0, g1;
     reaction<KIN>(kin, u, v, g0, g1);
-    const double d = sp.coeff[comp] * diffusion_smem<0>(sp, comp, Wc, rr, row, 0, t, N);
+    const double d = kc.coeff * diffusion_rows<0>(kc, rc, Wc, rr, t, N);
     return __dadd_rn(d, comp == 0 ? g0 : g1);
   };
 

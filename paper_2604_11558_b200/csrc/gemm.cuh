@@ -178,6 +178,10 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
     for (int kt = 0; kt < KT; ++kt, ++it) {
       const int st = it % STAGES;
       mbar_wait(&full[st], (it / STAGES) & 1);
+      // mma.sync.aligned needs the whole warp converged: lanes leave the
+      // try_wait poll independently, and lane 0 may still be in the
+      // previous tile's store block
+      __syncwarp();
       const double* sa = reinterpret_cast<const double*>(smem + st * STAGE);
       const double* sb = reinterpret_cast<const double*>(smem + st * STAGE + SA);
       if (VAR == VAR_TN) {
@@ -255,6 +259,11 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
     else if (tc > 0)
       mbar_wait(epi_empty, (tc - 1) & 1);  // previous tile's store has read etile
     bool bad = false;
+    // Partial tiles (the last m or n tile of an extent that BM/BN do not
+    // divide) are written straight from registers with bounds checks: the
+    // clipped bulk tensor store of such tiles measured nondeterministic on
+    // B200 with two CTAs per SM (tools/chain_dbg2.py); full tiles use TMA.
+    const bool full_tile = (m0 + BM <= p.M) && (n0 + BN <= p.N);
     // Phi1 operands for EPI_PHI (L2-resident table), all loads in flight per row group
     constexpr int EC = (MINB >= 2 && MT > 2) ? MT / 2 : MT;
 #pragma unroll
@@ -294,18 +303,28 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
             v1 = __dadd_rn(w2.y, __dmul_rn(p.tau, v1));
             bad |= !(fabs(v0) <= p.limit) || !(fabs(v1) <= p.limit);  // OOB entries are 0
           }
-          *slot = make_double2(v0, v1);
+          if (full_tile) {
+            *slot = make_double2(v0, v1);
+          } else {
+            const int m = m0 + ml, n = n0 + nl;
+            if (m < p.M && n < p.N)
+              *reinterpret_cast<double2*>(p.out + (long long)f * p.out_f + (long long)s * p.out_s +
+                                          (long long)m * p.ldc + n) = make_double2(v0, v1);
+          }
         }
       }
     }
     fence_proxy_async_smem();
     named_bar(1, NCW * 32);
     if (threadIdx.x == 0) {
-      tma_store_4d(&mapO, etile, n0, m0, s, f);  // clipped to the tensor bounds
-      bulk_commit();
-      bulk_wait_read0();
+      if (full_tile) {
+        tma_store_4d(&mapO, etile, n0, m0, s, f);
+        bulk_commit();
+        bulk_wait_read0();
+      }
       mbar_arrive(epi_empty);
     }
+    __syncwarp();  // reconverge warp 0 (lane 0 ran the store) before the next tile's MMAs
     if (EPI == EPI_AXPY) {
       if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(p.first_bad + f, step_now);
     }

@@ -111,10 +111,13 @@ int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   constexpr int smem = gemm_smem_bytes<BM, BN, ST>();
   constexpr int threads = (BM / WM) * (BN / WN) * 32 + 32;
   static int resident = 0;  // CTAs of this instantiation that fit on the chip at once
+  static int pad = 0;  // debugging: CURVIGPU_SMEM_PAD extra bytes per CTA (lowers occupancy)
   if (configure_only) {
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const char* ps = getenv("CURVIGPU_SMEM_PAD");
+    pad = ps ? atoi(ps) : 0;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem + pad));
     int per_sm = 0, dev = 0, sms = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem + pad));
     CUDA_TRY(cudaGetDevice(&dev));
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     resident = (per_sm > 0 ? per_sm : 1) * sms;
@@ -124,8 +127,9 @@ int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   if (tiles <= 0) return CG_OK;
   if (tiles > INT_MAX) return fail(CG_EUNSUPPORTED, "grid too large");
   // persistent grid: at most one wave of resident CTAs, each looping over tiles
-  const long long blocks = (resident > 0 && tiles > resident) ? resident : tiles;
-  kern<<<(unsigned)blocks, threads, smem, stream>>>(ma, mb, mw, mo, p);
+  long long blocks = (resident > 0 && tiles > resident) ? resident : tiles;
+  if (getenv("CURVIGPU_NOPERSIST")) blocks = tiles;
+  kern<<<(unsigned)blocks, threads, smem + pad, stream>>>(ma, mb, mw, mo, p);
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
 }
@@ -975,6 +979,14 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
 }
 
 int cg_plan_stage_count(const cg_plan* p) { return p ? (int)p->stages.size() : 0; }
+
+int cg_plan_copy_workspace(cg_plan* p, int which, double* dst, void* stream) {
+  if (!p || !dst || which < 0 || which > 2) return fail(CG_EINVAL, "bad workspace request");
+  const double* src = which == 0 ? p->X : which == 1 ? p->Y : p->S2;
+  CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)p->elems * sizeof(double), cudaMemcpyDeviceToDevice,
+                           static_cast<cudaStream_t>(stream)));
+  return CG_OK;
+}
 
 int cg_plan_stage_info(const cg_plan* p, int stage, long long* flops, long long* bytes) {
   if (!p || stage < -2 || stage >= (int)p->stages.size()) return fail(CG_EINVAL, "bad stage index");

@@ -148,40 +148,90 @@ __device__ __forceinline__ void stage_rows(double* s, const double* __restrict__
   }
 }
 
-// coeff-free diffusion action at interior row r (global row i), column l
+// Per-thread, per-component stencil coefficients, loaded once per CTA so the
+// inner loop issues no global loads (the first version re-read the bands for
+// every point and was LSU-bound).  Boundary terms carry a zero coefficient,
+// which leaves every value bit-identical to the branchy three-point form.
+struct CompCoef {
+  double coeff;
+  double th_diag, th_off;     // periodic theta stencil
+  double la, lb, lc, ld;      // contiguous-axis tridiagonal row (a, b, c_prev) and its metric weight
+};
+
+struct RowCoef {              // walked-axis tridiagonal row (shared by the CTA, in smem)
+  double a, b, c, d;          // a_i, b_i (0 at the last row), c_{i-1} (0 at the first), d_rho[i]
+};
+
 template <int GEOM>
-__device__ __forceinline__ double diffusion_smem(const StencilParams& p, int c, const double* s, int r, int i, int j,
-                                                 int l, int nl) {
+__device__ __forceinline__ CompCoef comp_coef(const StencilParams& p, int c, int l, int nl) {
+  CompCoef k;
+  k.coeff = p.coeff[c];
+  k.th_diag = p.th[2 * c];
+  k.th_off = p.th[2 * c + 1];
+  k.la = k.lb = k.lc = k.ld = 0.0;
+  if (GEOM != 0) {
+    const double* bands = (GEOM == 3) ? p.z_b + (long long)c * 3 * nl : p.phi_b + (long long)c * 3 * nl;
+    k.la = bands[l];
+    k.lb = (l < nl - 1) ? bands[nl + l] : 0.0;
+    k.lc = (l > 0) ? bands[2 * nl + l - 1] : 0.0;
+    if (GEOM == 1 || GEOM == 2) k.ld = p.d_phi[c * nl + l];
+  }
+  return k;
+}
+
+// coeff-free diffusion action at interior row r (global row i), column l,
+// from the shared-memory stage s (rows r, r+1, r+2 = i-1, i, i+1)
+template <int GEOM>
+__device__ __forceinline__ double diffusion_rows(const CompCoef& k, const RowCoef& rc, const double* s, int r, int l,
+                                                 int nl) {
   using S = FbuildShape<GEOM>;
   const double xm = s[r * nl + l], x0 = s[(r + 1) * nl + l], xp = s[(r + 2) * nl + l];
   int ll = l - 1, lr = l + 1;
   if (GEOM == 0) {  // periodic contiguous axis
     if (ll < 0) ll = nl - 1;
     if (lr >= nl) lr = 0;
+  } else {
+    if (ll < 0) ll = 0;  // coefficient is zero there
+    if (lr >= nl) lr = nl - 1;
   }
-  const double xl = (ll >= 0) ? s[(r + 1) * nl + ll] : 0.0;
-  const double xr = (lr < nl) ? s[(r + 1) * nl + lr] : 0.0;
-  const int n1 = p.n1;
+  const double xl = s[(r + 1) * nl + ll];
+  const double xr = s[(r + 1) * nl + lr];
   if (GEOM == 0) {  // disk: rho walked (tridiagonal), theta contiguous (periodic)
-    const double rr = tri3(p.rho_b + (long long)c * 3 * n1, n1, i, xm, x0, xp);
-    const double q = circ3(p.th + 2 * c, xl, x0, xr);
-    return rr + p.d_rho[c * n1 + i] * q;
+    const double rr = rc.a * x0 + rc.c * xm + rc.b * xp;
+    const double q = k.th_off * xl + k.th_diag * x0 + k.th_off * xr;
+    return rr + rc.d * q;
   } else if (GEOM == 1) {  // sphere: theta walked (periodic), phi contiguous (tridiagonal)
-    const double q = circ3(p.th + 2 * c, xm, x0, xp);
-    const double rr = tri3(p.phi_b + (long long)c * 3 * nl, nl, l, xl, x0, xr);
-    return q * p.d_phi[c * nl + l] + rr;
+    const double q = k.th_off * xm + k.th_diag * x0 + k.th_off * xp;
+    const double rr = k.la * x0 + k.lc * xl + k.lb * xr;
+    return q * k.ld + rr;
   } else {
     const double ym = s[(S::RB + 2 + r) * nl + l], yp = s[(2 * S::RB + 2 + r) * nl + l];
-    const double rr = tri3(p.rho_b + (long long)c * 3 * n1, n1, i, xm, x0, xp);
-    const double q = circ3(p.th + 2 * c, ym, x0, yp);
-    const double dr = p.d_rho[c * n1 + i];
-    if (GEOM == 2) {  // ball: phi contiguous (tridiagonal)
-      const double ph = tri3(p.phi_b + (long long)c * 3 * nl, nl, l, xl, x0, xr);
-      return rr + (dr * q) * p.d_phi[c * nl + l] + dr * ph;
-    } else {  // cylinder: z contiguous (tridiagonal)
-      const double z = tri3(p.z_b + (long long)c * 3 * nl, nl, l, xl, x0, xr);
-      return rr + dr * q + z;
+    const double rr = rc.a * x0 + rc.c * xm + rc.b * xp;
+    const double q = k.th_off * ym + k.th_diag * x0 + k.th_off * yp;
+    const double dr = rc.d;
+    const double t = k.la * x0 + k.lc * xl + k.lb * xr;
+    if (GEOM == 2) return rr + (dr * q) * k.ld + dr * t;  // ball: phi contiguous
+    return rr + dr * q + t;                                // cylinder: z contiguous
+  }
+}
+
+// fill the CTA's walked-axis row coefficients for components [0, nc)
+template <int GEOM>
+__device__ __forceinline__ void row_coefs(RowCoef* rcs, const StencilParams& p, int i0, int nc) {
+  using S = FbuildShape<GEOM>;
+  const int n1 = p.n1;
+  for (int idx = threadIdx.x; idx < nc * S::RB; idx += blockDim.x) {
+    const int c = idx / S::RB, r = idx - c * S::RB;
+    const int i = min(i0 + r, n1 - 1);
+    RowCoef rc{0.0, 0.0, 0.0, 0.0};
+    if (GEOM != 1) {
+      const double* bands = p.rho_b + (long long)c * 3 * n1;
+      rc.a = bands[i];
+      rc.b = (i < n1 - 1) ? bands[n1 + i] : 0.0;
+      rc.c = (i > 0) ? bands[2 * n1 + i - 1] : 0.0;
+      rc.d = p.d_rho[c * n1 + i];
     }
+    rcs[idx] = rc;
   }
 }
 
@@ -189,10 +239,12 @@ template <int GEOM, int KIN>
 __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p) {
   using S = FbuildShape<GEOM>;
   extern __shared__ double fb_smem[];
+  __shared__ RowCoef rcs[8 * S::RB];  // up to 8 components
   if (p.step && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *p.step += 1;
   const int nl = S::D3 ? p.n3 : p.n2;
   const int n1 = p.n1;
   const int l = threadIdx.x;
+  const int lcl = l < nl ? l : nl - 1;
   const int i0 = blockIdx.x * S::RB;
   const int j = S::D3 ? (int)blockIdx.y : 0;
   const int b = blockIdx.z;
@@ -201,31 +253,44 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
   const int plane = S::ROWS * nl;
 
   if (KIN == KIN_EXTERNAL) {
+    const int nc = p.ncomp < 8 ? p.ncomp : 8;
+    row_coefs<GEOM>(rcs, p, i0, nc);
     for (int c = 0; c < p.ncomp; ++c) {
       const double* X = p.W + run_base + (long long)c * p.npts;
       if (c > 0) __syncthreads();
       stage_rows<GEOM>(fb_smem, X, i0, j, n1, p.n2, nl, rs);
       __syncthreads();
       if (l < nl) {
+        const CompCoef k = comp_coef<GEOM>(p, c, l, nl);
 #pragma unroll
         for (int r = 0; r < S::RB; ++r) {
           const int i = i0 + r;
           if (i >= n1) break;
           const long long idx = run_base + (long long)c * p.npts + (long long)i * rs + l;
           double val = 0.0;
-          if (p.with_diffusion) val = p.coeff[c] * diffusion_smem<GEOM>(p, c, fb_smem, r, i, j, l, nl);
+          if (p.with_diffusion) val = k.coeff * diffusion_rows<GEOM>(k, rcs[(c < 8 ? c : 7) * S::RB + r], fb_smem, r, l, nl);
           if (p.with_reaction) val = p.with_diffusion ? __dadd_rn(val, __ldg(p.G + idx)) : __ldg(p.G + idx);
           p.F[idx] = val;
         }
       }
     }
   } else {
+    const bool with_d = p.with_diffusion;
+    if (with_d) row_coefs<GEOM>(rcs, p, i0, 2);
     stage_rows<GEOM>(fb_smem, p.W + run_base, i0, j, n1, p.n2, nl, rs);
     stage_rows<GEOM>(fb_smem + plane, p.W + run_base + p.npts, i0, j, n1, p.n2, nl, rs);
+    CompCoef k0{}, k1{};  // operator coefficients are only present when diffusing
+    if (with_d) {
+      k0 = comp_coef<GEOM>(p, 0, lcl, nl);
+      k1 = comp_coef<GEOM>(p, 1, lcl, nl);
+    }
+    double kin[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) kin[q] = (q < p.nparams) ? p.kin[(long long)b * p.nparams + q] : 0.0;
+    const double lift0 = p.lift[0], lift1 = p.lift[1];
+    const bool with_r = p.with_reaction;
     __syncthreads();
     if (l >= nl) return;
-    const double* kin = p.kin + (long long)b * p.nparams;
-    const double lift0 = p.lift[0], lift1 = p.lift[1];
     double* __restrict__ Fo = p.F;
 #pragma unroll
     for (int r = 0; r < S::RB; ++r) {
@@ -233,18 +298,18 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
       if (i >= n1) break;
       const long long off = run_base + (long long)i * rs + l;
       double g0 = 0.0, g1 = 0.0;
-      if (p.with_reaction) {
+      if (with_r) {
         double u = fb_smem[(r + 1) * nl + l], v = fb_smem[plane + (r + 1) * nl + l];
         if (lift0 != 0.0) u = __dadd_rn(u, lift0);
         if (lift1 != 0.0) v = __dadd_rn(v, lift1);
         reaction<KIN>(kin, u, v, g0, g1);
       }
       double fu = g0, fv = g1;
-      if (p.with_diffusion) {
-        const double du = p.coeff[0] * diffusion_smem<GEOM>(p, 0, fb_smem, r, i, j, l, nl);
-        const double dv = p.coeff[1] * diffusion_smem<GEOM>(p, 1, fb_smem + plane, r, i, j, l, nl);
-        fu = p.with_reaction ? __dadd_rn(du, g0) : du;
-        fv = p.with_reaction ? __dadd_rn(dv, g1) : dv;
+      if (with_d) {
+        const double du = k0.coeff * diffusion_rows<GEOM>(k0, rcs[r], fb_smem, r, l, nl);
+        const double dv = k1.coeff * diffusion_rows<GEOM>(k1, rcs[S::RB + r], fb_smem + plane, r, l, nl);
+        fu = with_r ? __dadd_rn(du, g0) : du;
+        fv = with_r ? __dadd_rn(dv, g1) : dv;
       }
       Fo[off] = fu;
       Fo[off + p.npts] = fv;

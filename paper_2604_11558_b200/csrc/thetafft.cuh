@@ -303,7 +303,17 @@ __device__ __forceinline__ void dit_stage(double2* a) {
     if (j != 0) {
       const int t = j * (16 / LEN);
       const double c = cos16(t), s = INV ? sin16(t) : -sin16(t);
-      v = make_double2(v.x * c - v.y * s, v.x * s + v.y * c);
+      if (t == 4) {
+        v = INV ? make_double2(-v.y, v.x) : make_double2(v.y, -v.x);  // w = +-i: free
+      } else if (t == 2 || t == 6) {
+        // |c| = |s| = sqrt(1/2): two adds and two multiplies
+        const double h = 0.7071067811865476;
+        const double re = (c > 0 ? v.x : -v.x) - (s > 0 ? v.y : -v.y);
+        const double im = (s > 0 ? v.x : -v.x) + (c > 0 ? v.y : -v.y);
+        v = make_double2(h * re, h * im);
+      } else {
+        v = make_double2(v.x * c - v.y * s, v.x * s + v.y * c);
+      }
     }
     a[st + j] = make_double2(u.x + v.x, u.y + v.y);
     a[st + j + half] = make_double2(u.x - v.x, u.y - v.y);

@@ -377,6 +377,15 @@ class SplitPlan:
             _native.check(n, "cg_plan_step_kernels")
         return [ids[i] for i in range(min(n, 32))]
 
+    def workspace(self, which: int):
+        """Copy of workspace X (0), Y (1) or the second state buffer (2)."""
+        import torch
+
+        out = torch.empty(self.state_shape, dtype=torch.float64, device="cuda")
+        _native.check(self._lib.cg_plan_copy_workspace(self._h, int(which), out.data_ptr(), self._stream()),
+                      "cg_plan_copy_workspace")
+        return out
+
     def run_stage(self, stage: int, W, out):
         self._check_state(W, "W")
         self._check_state(out, "out")

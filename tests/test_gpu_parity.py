@@ -269,3 +269,23 @@ def test_kinetics_kernel_bitwise_vs_oracle(kind, params):
         ref = orc.kinetics(kind, params, {"u": W[b, 0], "v": W[b, 1]}, ["u", "v"], [0.25, -0.5])
         assert np.array_equal(got[b, 0], ref["u"]), kind
         assert np.array_equal(got[b, 1], ref["v"]), kind
+
+
+def test_full_size_ball_reruns_bitwise_identical():
+    """Regression guard: partial tiles (n = 100) under the persistent,
+    two-CTA-per-SM GEMM once produced run-to-run differences (a clipped bulk
+    tensor store; see csrc/gemm.cuh)."""
+    import torch
+
+    sysm = pcfg.config4()
+    geos = [prepare(c.ops, 1e-2) for c in sysm.components]
+    plan = SplitPlan(geos, 1, sysm.kinetics.kind, sysm.kinetics.param_vector()[None, :])
+    W = torch.from_numpy(np.stack([c.initial for c in sysm.components])[None]).cuda()
+    bad = torch.full((1, 2), INT32_MAX, dtype=torch.int32, device="cuda")
+    outs = []
+    for _ in range(4):
+        s = W.clone()
+        plan.run(s, 0, 40, bad)
+        outs.append(s.cpu())
+    for o in outs[1:]:
+        assert torch.equal(outs[0], o)
