@@ -219,11 +219,12 @@ def theta_variants(ens, init_dev, chunk, stream):
     return out
 
 
-def ncu_traffic(kernel_key):
-    """Per-launch dram bytes of a kernel from the committed ncu summary, or None."""
+def ncu_traffic(kernel_key, theta):
+    """Per-launch DRAM bytes (read + write) of a kernel from the committed ncu
+    capture of one config-5 step (profiles/ncu_traffic.json), or None."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     try:
-        return json.loads(p.read_text()).get(kernel_key)
+        return json.loads(p.read_text()).get(f"{theta}:{kernel_key}")
     except Exception:
         return None
 
@@ -372,7 +373,7 @@ def engine_arm(args):
         "fp64_frac_of_peak_step": gemm_flops / (hi - lo) * RUNS * chunk * args.steps / dev_sec / 1e12
         / (FP64_PEAK_TFLOPS * world),
         "roofline": {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
-                     "frac": dom["frac"], "traffic": ncu_traffic(dom["kernel"]), "kernel": dom["kernel"],
+                     "frac": dom["frac"], "traffic": ncu_traffic(dom["kernel"], args.theta), "kernel": dom["kernel"],
                      "peak_source": ("measured DMMA peak, profiles/r01_fp64_peak.txt (MEASURED_PEAKS.json has "
                                      "no fp64 figure)") if dom["bound"] == "tensor" else "MEASURED_PEAKS.json hbm_gbs"},
         "kernels": rows,
