@@ -21,6 +21,10 @@
  *                                                     integrators.py:413-427
  *                       (kinetics from the common state, step every
  *                        component, divergence guard DIVERGENCE_LIMIT :33)
+ *   cg_coupled_*        replace the closures of the bulk-surface models
+ *                       _build_ball / _build_cylinder   models.py:570-661
+ *                       (coupling terms models.py:322-369) and their
+ *                       run_simulation loop              integrators.py:413-427
  *   cg_rng_*            replaces Xoshiro256pp / Uniform / Normal
  *                                                     models.py:55-130
  *
@@ -164,6 +168,51 @@ int cg_plan_stage_info(const cg_plan* plan, int stage, long long* flops, long lo
 int cg_run_stage(cg_plan* plan, int stage, const double* W, double* W_out, int* first_bad, void* stream);
 /* Copy a plan workspace (0 = X, 1 = Y, 2 = second state) to dst (debugging / tests). */
 int cg_plan_copy_workspace(cg_plan* plan, int which, double* dst, void* stream);
+
+/* step_split with external G plus the divergence guard: like cg_step, but the
+ * guard records into first_bad with the plan's step counter, which this call
+ * advances by one (building block of coupled time loops; graph-capturable). */
+int cg_step_guarded(cg_plan* plan, const double* W, const double* G, double* W_out, int* first_bad,
+                    void* stream);
+/* Set the plan's device step counter (the next guarded step is step + 1). */
+int cg_plan_set_step(cg_plan* plan, long long step, void* stream);
+
+/* ---- bulk-surface coupled models ----
+ * Reaction terms of the reference's two mixed-geometry models from the common
+ * state: bulk (u, v) on a ball or cylinder, surface (r, s) on the sphere or
+ * the bottom disk, coupled through the bulk trace (outermost rho slice /
+ * z = 0 slice) with Robin / flux sources (models.py:322-369, :570-661).
+ *   CG_BS_BALL      params: alpha1 alpha2 beta1 zeta1 zeta2 zeta3 eta1 eta2;
+ *                   geom = {h_rho, rho_edge}
+ *   CG_BS_CYLINDER  params: alpha1 alpha2 alpha3 beta1 beta2 beta3 delta
+ *                   zeta1 zeta2 zeta3 zeta4 zeta5 eta1 eta2 eta3 eta5;
+ *                   geom = {h_z, 0}
+ * Wb/Gb are [2][bulk] (u, v), Ws/Gs are [2][surface] (r, s) device arrays;
+ * lift[] restores physical values (u, v, r, s). */
+#define CG_BS_BALL 1
+#define CG_BS_CYLINDER 2
+typedef struct {
+  int kind;
+  int nb[3];
+  int ns[2];
+  const double* params;
+  int nparams;
+  double geom[2];
+  double lift[4];
+} cg_coupling_desc;
+typedef struct cg_coupling cg_coupling;
+int cg_coupling_create(const cg_coupling_desc* desc, cg_coupling** out);
+void cg_coupling_destroy(cg_coupling* c);
+int cg_coupled_kinetics(cg_coupling* c, const double* Wb, const double* Ws, double* Gb, double* Gs, void* stream);
+/* The coupled time loop (run_simulation, integrators.py:413-427, for the
+ * four-component bulk-surface systems): per step the coupled reaction terms
+ * from the common state, then step_split of the bulk pair (plan `bulk`,
+ * geometry ball / cylinder) and of the surface pair (plan `surf`, sphere /
+ * disk), both created with batch 1, ncomp 2 and CG_KIN_EXTERNAL.  Wb / Ws
+ * advance in place; first_bad[4] (u, v, r, s) as in cg_run.  Replayed from
+ * CUDA graphs; the surface chain runs on a forked stream inside the graph. */
+int cg_coupled_run(cg_coupling* c, cg_plan* bulk, cg_plan* surf, double* Wb, double* Ws, long long step0,
+                   long long nsteps, int* first_bad, void* stream);
 
 /* Last error message of the calling thread. */
 const char* cg_last_error(void);

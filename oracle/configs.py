@@ -17,6 +17,7 @@ from .curvi_oracle import (
     System,
     Xoshiro,
     anomalous_stencil,
+    axial_stencil_nd,
     axial_stencil_nn,
     draw,
     fortran_fill,
@@ -135,6 +136,65 @@ def config5_member(i, dims=None, runs=512, initial=None, lam=-1.95):
              Comp("v", "disk", 10.0, rho=rho, theta=th, rho_weights=weights,
                   initial=initial[1], lift=ve)]
     return System(comps, "schnakenberg", {"gamma": ensemble_gamma(i, runs), "a": 0.1, "b": 0.9})
+
+
+# published defaults of the two bulk-surface models (src/models.py:178-213)
+BS_BALL_PARAMS = {"alpha1": 55.0, "alpha2": 0.1, "beta1": 0.9, "zeta1": 55.0, "zeta2": 5.0 / 12.0,
+                  "zeta3": 5.0 / 12.0, "eta1": 5.0, "eta2": 5.0, "delta": 10.0, "epsilon": 10.0}
+BS_CYL_PARAMS = {"alpha1": 1.0, "alpha2": 1.0, "alpha3": 0.15, "beta1": 1.0, "beta2": 1.0,
+                 "beta3": 0.15, "delta": 1.0, "epsilon": 20.0, "zeta1": 1.0, "zeta2": 10.0,
+                 "zeta3": 1.0, "zeta4": 66.0, "zeta5": 0.5, "eta1": 3.0, "eta2": 2.5,
+                 "eta3": 0.2, "eta5": 1.5}
+
+
+def bs_ball(dims, seed=1, initial=None, rho_star=1.0, params=None):
+    """bulk_surface_schnakenberg_ball (src/models.py:570-611): ball u, v and
+    sphere r, s, no lift; IC = equilibrium + Normal(1e-3) drawn u, v, r, s
+    from one generator (src/models.py:236-237, :412-432).  ``dims`` =
+    (n_rho, n_theta, n_phi)."""
+    p = dict(BS_BALL_PARAMS, **(params or {}))
+    n1, n2, n3 = dims
+    rho = radial_stencil(3, n1, rho_star)
+    th = theta_stencil(n2)
+    ph = polar_stencil(n3)
+    ue = p["alpha2"] + p["beta1"]
+    ve = p["beta1"] / ue**2
+    if initial is None:
+        rng = Xoshiro(seed)
+        initial = []
+        for shape, base in (((n1, n2, n3), ue), ((n1, n2, n3), ve), ((n2, n3), ue), ((n2, n3), ve)):
+            f = np.full(shape, base)
+            f += fortran_fill(draw(rng, ("normal", 1e-3), int(np.prod(shape))), shape)
+            initial.append(f)
+    comps = [Comp("u", "ball", 1.0, rho=rho, theta=th, phi=ph, initial=initial[0]),
+             Comp("v", "ball", p["delta"], rho=rho, theta=th, phi=ph, initial=initial[1]),
+             Comp("r", "sphere", 1.0 / rho_star**2, theta=th, phi=ph, initial=initial[2]),
+             Comp("s", "sphere", p["epsilon"] / rho_star**2, theta=th, phi=ph, initial=initial[3])]
+    return System(comps, "bs_ball", dict(p, h=rho.h, rho_edge=rho.grid[-1]))
+
+
+def bs_cylinder(dims, seed=1, initial=None, rho_star=25.0, z_star=25.0, params=None):
+    """bsdib_cylinder (src/models.py:614-661): cylinder u, v (lifted by the
+    equilibrium alpha2, beta2; no perturbation) and bottom-disk r, s
+    (Uniform(0, 1e-2)).  ``dims`` = (n_rho, n_theta, n_z)."""
+    p = dict(BS_CYL_PARAMS, **(params or {}))
+    n1, n2, n3 = dims
+    rho = radial_stencil(2, n1, rho_star)
+    th = theta_stencil(n2)
+    z = axial_stencil_nd(n3, z_star)
+    ue, ve = p["alpha2"], p["beta2"]
+    if initial is None:
+        rng = Xoshiro(seed)
+        initial = [np.zeros((n1, n2, n3)), np.zeros((n1, n2, n3))]
+        for base in (0.0, p["zeta5"]):
+            f = np.full((n1, n2), base)
+            f += fortran_fill(draw(rng, ("uniform", 0.0, 1e-2), n1 * n2), (n1, n2))
+            initial.append(f)
+    comps = [Comp("u", "cylinder", 1.0, rho=rho, theta=th, z=z, initial=initial[0], lift=ue),
+             Comp("v", "cylinder", p["delta"], rho=rho, theta=th, z=z, initial=initial[1], lift=ve),
+             Comp("r", "disk", 1.0, rho=rho, theta=th, initial=initial[2]),
+             Comp("s", "disk", p["epsilon"], rho=rho, theta=th, initial=initial[3])]
+    return System(comps, "bs_cylinder", dict(p, h=z.h))
 
 
 BUILDERS = {1: config1, 2: config2, 3: config3, 4: config4}

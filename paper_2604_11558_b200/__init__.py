@@ -6,7 +6,7 @@ operation in hand-written sm_100a CUDA (libcurvigpu.so, C ABI in
 include/curvigpu.h) called through ctypes on PyTorch-owned device memory.
 """
 
-from . import configs, ensemble, integrators, models, operators, phifun  # noqa: F401
+from . import configs, coupled, ensemble, integrators, models, operators, phifun  # noqa: F401
 from ._native import LIB_PATH, EngineError  # noqa: F401
 
 __version__ = "0.1.0"

@@ -79,7 +79,28 @@ EXPORTS = (
     "cg_run_stage",
     "cg_plan_step_kernels",
     "cg_plan_copy_workspace",
+    "cg_step_guarded",
+    "cg_plan_set_step",
+    "cg_coupling_create",
+    "cg_coupling_destroy",
+    "cg_coupled_kinetics",
+    "cg_coupled_run",
 )
+
+CG_BS_BALL = 1
+CG_BS_CYLINDER = 2
+
+
+class cg_coupling_desc(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int),
+        ("nb", ctypes.c_int * 3),
+        ("ns", ctypes.c_int * 2),
+        ("params", ctypes.POINTER(ctypes.c_double)),
+        ("nparams", ctypes.c_int),
+        ("geom", ctypes.c_double * 2),
+        ("lift", ctypes.c_double * 4),
+    ]
 
 
 def lib():
@@ -134,6 +155,18 @@ def lib():
     L.cg_plan_step_kernels.restype = ctypes.c_int
     L.cg_plan_copy_workspace.argtypes = [vp, ctypes.c_int, vp, vp]
     L.cg_plan_copy_workspace.restype = ctypes.c_int
+    L.cg_step_guarded.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.cg_step_guarded.restype = ctypes.c_int
+    L.cg_plan_set_step.argtypes = [vp, ctypes.c_longlong, vp]
+    L.cg_plan_set_step.restype = ctypes.c_int
+    L.cg_coupling_create.argtypes = [ctypes.POINTER(cg_coupling_desc), ctypes.POINTER(vp)]
+    L.cg_coupling_create.restype = ctypes.c_int
+    L.cg_coupling_destroy.argtypes = [vp]
+    L.cg_coupling_destroy.restype = None
+    L.cg_coupled_kinetics.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.cg_coupled_kinetics.restype = ctypes.c_int
+    L.cg_coupled_run.argtypes = [vp, vp, vp, vp, vp, ctypes.c_longlong, ctypes.c_longlong, vp, vp]
+    L.cg_coupled_run.restype = ctypes.c_int
     _lib = L
     return L
 

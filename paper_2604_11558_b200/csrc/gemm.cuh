@@ -279,8 +279,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
           for (int j = 0; j < NT; ++j) {
             int n = n0 + wn0 + j * 8 + col_in8;
             if (n >= p.N) n = 0;
+            const int n_hi = (n + 1 < p.N) ? n + 1 : n;  // odd N: the pair's second column is padding
             ph[ii][j].x = __ldg(phirow + (long long)n * p.phi_n);
-            ph[ii][j].y = __ldg(phirow + (long long)(n + 1) * p.phi_n);
+            ph[ii][j].y = __ldg(phirow + (long long)n_hi * p.phi_n);
           }
         }
       }

@@ -24,6 +24,7 @@
 #include "stencil.cuh"
 #include "thetafft.cuh"
 #include "fused_disk.cuh"
+#include "coupling.cuh"
 
 using namespace cg;
 
@@ -164,6 +165,18 @@ int launch_gemm(int var, int epi, int cfg, const Maps& m, const GemmParams& p, c
 
 __global__ void set_step_kernel(int* step, int value) { *step = value; }
 
+// rows of nl values from row stride lds to row stride ldd (padded <-> caller layout)
+__global__ void repack_kernel(const double* __restrict__ src, int lds, double* __restrict__ dst, int ldd,
+                              long long rows, int nl) {
+  const long long total = rows * nl;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long r = t / nl;
+    const int k = (int)(t - r * nl);
+    dst[r * ldd + k] = src[r * lds + k];
+  }
+}
+
 template <int GEOM, int KIN>
 int launch_fbuild_t(const StencilParams& p, cudaStream_t s, bool configure_only) {
   using S = FbuildShape<GEOM>;
@@ -217,6 +230,7 @@ constexpr int VAR_THETA = 2;  // FFT theta propagator (thetafft.cuh), not a GEMM
 struct Stage {
   int var, epi, cfg;
   int M, N, K, nslab;
+  int ldr;       // row stride of the contiguous dim of the state views (K for TN, N for NN and the output)
   int src, dst;  // BUF_X / BUF_Y / BUF_OUT
   const double* phi;
   long long phi_c, phi_s;
@@ -241,7 +255,16 @@ constexpr int kChunk = 16;  // steps per captured graph (even)
 struct cg_plan {
   int geom, n1, n2, n3, B, C, kin, P;
   double tau;
-  long long npts, elems;
+  // Storage layout: the contiguous (last) axis of logical extent nl is stored
+  // with row stride ld = even(nl) so every TMA row stride is a multiple of 16
+  // bytes.  npts / elems count storage elements, npts_u / elems_u the user's
+  // unpadded arrays.  When padded, cg_run / cg_step repack the caller's
+  // arrays into S0 (ghost column held at zero, never read by TMA: every map
+  // declares the logical extent).
+  int nl = 0, ld = 0;
+  bool padded = false;
+  long long npts, elems, npts_u = 0, elems_u = 0;
+  double* S0 = nullptr;
   std::vector<void*> allocs;
   double *coeff = nullptr, *lift = nullptr, *kin_params = nullptr;
   double *rho_b = nullptr, *phi_b = nullptr, *z_b = nullptr, *th = nullptr, *d_rho = nullptr, *d_phi = nullptr;
@@ -338,6 +361,13 @@ int add_stage(cg_plan* p, int var, int epi, int M, int N, int K, int nslab, int 
   st.src = src;
   st.dst = dst;
   st.phi_rdiv = 1;
+  st.ldr = p->ld;
+  if (var == VAR_NN && p->n3 > 1 && nslab == 1 && N == p->n2 * p->n3) {
+    // first-mode product over flattened (theta, last) columns: the padded
+    // columns ride along (they hold zeros and only ever produce zeros)
+    st.N = p->n2 * p->ld;
+    st.ldr = st.N;
+  }
   const long long nbatch = (long long)p->B * p->C * nslab;
   st.cfg = pick_cfg(var, nbatch, M, N, (int)p->stages.size());
   double* op = nullptr;
@@ -417,6 +447,8 @@ int launch_fstage(cg_plan* p, const double* Win, const double* Gext, bool fused_
   sp.lift = p->lift;
   sp.kin = p->kin_params;
   sp.nparams = p->P;
+  sp.ldw = sp.ldf = p->ld;
+  sp.npw = sp.npf = p->npts;
   sp.W = Win;
   sp.G = Gext;
   sp.F = p->X;
@@ -489,13 +521,13 @@ int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
     if (st.var == VAR_TN) {
       // state as (K, rows, field)
       const uint64_t dims[3] = {(uint64_t)st.K, (uint64_t)st.M, (uint64_t)nfield};
-      const uint64_t strides[2] = {(uint64_t)st.K * 8, (uint64_t)p->npts * 8};
+      const uint64_t strides[2] = {(uint64_t)st.ldr * 8, (uint64_t)p->npts * 8};
       const uint32_t box[3] = {16, (uint32_t)tc.BM, 1};
       rc = make_map(&smap, src, 3, dims, strides, box);
     } else {
       // state as (N, K, slab, field)
       const uint64_t dims[4] = {(uint64_t)st.N, (uint64_t)st.K, (uint64_t)st.nslab, (uint64_t)nfield};
-      const uint64_t strides[3] = {(uint64_t)st.N * 8, (uint64_t)st.K * st.N * 8, (uint64_t)p->npts * 8};
+      const uint64_t strides[3] = {(uint64_t)st.ldr * 8, (uint64_t)st.K * st.ldr * 8, (uint64_t)p->npts * 8};
       const uint32_t box[4] = {16, 16, 1, 1};
       rc = make_map(&smap, src, 4, dims, strides, box);
     }
@@ -511,8 +543,8 @@ int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
     gp.tiles_n = (st.N + tc.BN - 1) / tc.BN;
     gp.out = dst;
     gp.out_f = p->npts;
-    gp.out_s = (long long)st.K * st.N;  // slab stride (NN middle mode: n2*n3 ... K*N)
-    gp.ldc = st.N;
+    gp.out_s = (long long)st.K * st.ldr;  // slab stride (NN middle mode: K rows of ldr)
+    gp.ldc = st.ldr;
     gp.w = Win;
     gp.phi = st.phi;
     gp.phi_c = st.phi_c;
@@ -530,8 +562,8 @@ int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
     {
       // output (and, for the axpy epilogue, the previous state) as (N, M, slab, field), (BN, BM) boxes
       const uint64_t dims[4] = {(uint64_t)st.N, (uint64_t)st.M, (uint64_t)st.nslab, (uint64_t)nfield};
-      const uint64_t slab = st.nslab > 1 ? (uint64_t)gp.out_s : (uint64_t)st.M * st.N;
-      const uint64_t strides[3] = {(uint64_t)st.N * 8, slab * 8, (uint64_t)p->npts * 8};
+      const uint64_t slab = st.nslab > 1 ? (uint64_t)gp.out_s : (uint64_t)st.M * st.ldr;
+      const uint64_t strides[3] = {(uint64_t)st.ldr * 8, slab * 8, (uint64_t)p->npts * 8};
       const uint32_t box[4] = {(uint32_t)tc.BN, (uint32_t)tc.BM, 1, 1};
       if ((rc = make_map(&mp.o, dst, 4, dims, strides, box, false))) return rc;
       if (st.epi == EPI_AXPY) {
@@ -610,6 +642,15 @@ int launch_fused_front(cg_plan* p, const double* Win, bool count_step, cudaStrea
 }
 
 // Launch one full step: Win (+G) -> F -> stage chain -> Wout.
+int repack(const cg_plan* p, const double* src, int lds, double* dst, int ldd, cudaStream_t s) {
+  const long long rows = p->elems_u / p->nl;
+  const long long total = p->elems_u;
+  const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 148LL * 16);
+  repack_kernel<<<blocks, 256, 0, s>>>(src, lds, dst, ldd, rows, p->nl);
+  CUDA_TRY(cudaGetLastError());
+  return CG_OK;
+}
+
 int launch_step(cg_plan* p, const double* Win, double* Wout, const double* Gext, bool fused_kin, int* first_bad,
                 bool count_step, cudaStream_t s) {
   int rc;
@@ -627,7 +668,7 @@ int launch_step(cg_plan* p, const double* Win, double* Wout, const double* Gext,
 
 // Decide whether the disk front end can run fused (after build_stages).
 int setup_fused_front(cg_plan* p) {
-  if (p->geom != CG_DISK || p->kin == CG_KIN_EXTERNAL || p->C != 2 || p->stages.empty() ||
+  if (p->geom != CG_DISK || p->padded || p->kin == CG_KIN_EXTERNAL || p->C != 2 || p->stages.empty() ||
       p->stages[0].var != VAR_THETA || !getenv("CURVIGPU_FUSED_FRONT"))
     return CG_OK;
   const int M = p->n2 / 2;
@@ -657,7 +698,8 @@ int build_stages(cg_plan* p, const cg_desc* d) {
   int rc = 0;
   // phi tables
   auto up_phi = [&](const double* h, size_t per, double** out) -> int { return upload(p, h, per * C, out); };
-  const bool fft = (d->options & CG_OPT_THETA_FFT) != 0;
+  // the FFT theta kernels address unpadded fields: padded plans keep the GEMM pair
+  const bool fft = (d->options & CG_OPT_THETA_FFT) != 0 && !p->padded;
   if (p->geom == CG_DISK && fft && pow2(n2)) {
     if ((rc = need(d->phi1_rho, "phi1_rho")) || (rc = need(d->Phi, "Phi"))) return rc;
     const double *Ph = d->Phi, *P1 = d->phi1_rho;
@@ -849,7 +891,7 @@ extern "C" {
 const char* cg_last_error(void) { return g_err.c_str(); }
 int cg_version(void) { return 1; }
 
-long long cg_plan_state_elems(const cg_plan* plan) { return plan ? plan->elems : 0; }
+long long cg_plan_state_elems(const cg_plan* plan) { return plan ? plan->elems_u : 0; }
 
 void cg_plan_destroy(cg_plan* p) {
   if (!p) return;
@@ -870,9 +912,6 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
   if (d->kinetics != CG_KIN_EXTERNAL && d->ncomp != 2)
     return fail(CG_EUNSUPPORTED, "built-in kinetics kinds are two-species");
   if (d->kinetics < CG_KIN_EXTERNAL || d->kinetics > CG_KIN_DIB) return fail(CG_EUNSUPPORTED, "unknown kinetics");
-  const int nlast = is3d ? d->n[2] : d->n[1];
-  if (nlast % 2 != 0)
-    return fail(CG_EUNSUPPORTED, "the contiguous (last) axis must have even extent (TMA 16-byte row strides)");
   if (!(d->tau >= 0.0)) return fail(CG_EINVAL, "tau must be nonnegative");
   if (!d->coeff || !d->lift) return fail(CG_EINVAL, "coeff and lift are required");
 
@@ -886,8 +925,13 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
   p->kin = d->kinetics;
   p->P = d->nparams;
   p->tau = d->tau;
-  p->npts = (long long)p->n1 * p->n2 * p->n3;
+  p->nl = is3d ? p->n3 : p->n2;
+  p->ld = (p->nl + 1) & ~1;
+  p->padded = p->ld != p->nl;
+  p->npts_u = (long long)p->n1 * p->n2 * p->n3;
+  p->npts = p->npts_u / p->nl * p->ld;
   p->elems = p->npts * p->B * p->C;
+  p->elems_u = p->npts_u * p->B * p->C;
 
   int rc = CG_OK;
   auto bail = [&](int code) {
@@ -965,6 +1009,13 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
   if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&p->X)))) return bail(rc);
   if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&p->Y)))) return bail(rc);
   if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&p->S2)))) return bail(rc);
+  if (p->padded) {
+    if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&p->S0)))) return bail(rc);
+    for (double* buf : {p->X, p->Y, p->S2, p->S0}) {
+      cudaError_t e0 = cudaMemset(buf, 0, bytes);
+      if (e0 != cudaSuccess) return bail(fail(CG_ECUDA, cudaGetErrorString(e0)));
+    }
+  }
   if ((rc = dev_alloc(p, sizeof(int), reinterpret_cast<void**>(&p->step_dev)))) return bail(rc);
   if ((rc = dev_alloc(p, sizeof(int) * (size_t)p->B * C, reinterpret_cast<void**>(&p->scratch_bad))))
     return bail(rc);
@@ -983,6 +1034,7 @@ int cg_plan_stage_count(const cg_plan* p) { return p ? (int)p->stages.size() : 0
 int cg_plan_copy_workspace(cg_plan* p, int which, double* dst, void* stream) {
   if (!p || !dst || which < 0 || which > 2) return fail(CG_EINVAL, "bad workspace request");
   const double* src = which == 0 ? p->X : which == 1 ? p->Y : p->S2;
+  if (p->padded) return repack(p, src, p->ld, dst, p->nl, static_cast<cudaStream_t>(stream));
   CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)p->elems * sizeof(double), cudaMemcpyDeviceToDevice,
                            static_cast<cudaStream_t>(stream)));
   return CG_OK;
@@ -992,13 +1044,13 @@ int cg_plan_stage_info(const cg_plan* p, int stage, long long* flops, long long*
   if (!p || stage < -2 || stage >= (int)p->stages.size()) return fail(CG_EINVAL, "bad stage index");
   if (stage < 0) {  // F-build, or the fused F-build + theta kernel: read W once, write F (T) once
     if (flops) *flops = 0;
-    if (bytes) *bytes = 2LL * p->elems * (long long)sizeof(double);  // read W once, write F once
+    if (bytes) *bytes = 2LL * p->elems_u * (long long)sizeof(double);  // read W once, write F once
     return CG_OK;
   }
   const Stage& st = p->stages[stage];
   const long long items = (long long)p->B * p->C * st.nslab;
   if (flops) *flops = 2LL * st.M * st.N * st.K * items;
-  if (bytes) *bytes = (st.epi == EPI_AXPY ? 3LL : 2LL) * p->elems * (long long)sizeof(double);
+  if (bytes) *bytes = (st.epi == EPI_AXPY ? 3LL : 2LL) * p->elems_u * (long long)sizeof(double);
   return CG_OK;
 }
 
@@ -1024,6 +1076,7 @@ int cg_run_stage(cg_plan* p, int stage, const double* W, double* W_out, int* fir
   if (!p || !W || !W_out) return fail(CG_EINVAL, "null argument");
   if (stage < -2 || stage >= (int)p->stages.size()) return fail(CG_EINVAL, "bad stage index");
   if (stage == -2 && !p->fused_front) return fail(CG_EINVAL, "plan has no fused front kernel");
+  if (p->padded) return fail(CG_EUNSUPPORTED, "per-stage access needs an even contiguous axis");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (stage == -2) return launch_fused_front(p, W, false, s);
   if (stage < 0) return launch_fstage(p, W, nullptr, p->kin != CG_KIN_EXTERNAL, false, s);
@@ -1048,6 +1101,8 @@ int cg_apply_diffusion(cg_plan* p, const double* W, double* out, void* stream) {
   sp.d_phi = p->d_phi;
   sp.coeff = p->coeff;
   sp.lift = p->lift;
+  sp.ldw = sp.ldf = p->nl;  // caller's unpadded arrays
+  sp.npw = sp.npf = p->npts_u;
   sp.W = W;
   sp.F = out;
   sp.with_diffusion = 1;
@@ -1069,6 +1124,8 @@ int cg_kinetics(cg_plan* p, const double* W, double* G, void* stream) {
   sp.lift = p->lift;
   sp.kin = p->kin_params;
   sp.nparams = p->P;
+  sp.ldw = sp.ldf = p->nl;
+  sp.npw = sp.npf = p->npts_u;
   sp.W = W;
   sp.F = G;
   sp.with_diffusion = 0;
@@ -1077,18 +1134,247 @@ int cg_kinetics(cg_plan* p, const double* W, double* G, void* stream) {
 }
 
 int cg_step(cg_plan* p, const double* W, const double* G, double* W_out, void* stream) {
-  if (!p || !W || !G || !W_out) return fail(CG_EINVAL, "null argument");
-  if (W == W_out) return fail(CG_EINVAL, "W_out must not alias W");
-  return launch_step(p, W, W_out, G, false, p->scratch_bad, false, static_cast<cudaStream_t>(stream));
+  return cg_step_guarded(p, W, G, W_out, p ? p->scratch_bad : nullptr, stream);
 }
 
-int cg_run(cg_plan* p, double* state, long long step0, long long nsteps, int* first_bad, void* stream) {
-  if (!p || !state || !first_bad) return fail(CG_EINVAL, "null argument");
+int cg_step_guarded(cg_plan* p, const double* W, const double* G, double* W_out, int* first_bad, void* stream) {
+  if (!p || !W || !G || !W_out || !first_bad) return fail(CG_EINVAL, "null argument");
+  if (W == W_out) return fail(CG_EINVAL, "W_out must not alias W");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool count = first_bad != p->scratch_bad;
+  if (!p->padded) return launch_step(p, W, W_out, G, false, first_bad, count, s);
+  // padded storage: W -> S0, G -> S2 (consumed by the F-build before the last stage writes S2)
+  int rc;
+  if ((rc = repack(p, W, p->nl, p->S0, p->ld, s)) || (rc = repack(p, G, p->nl, p->S2, p->ld, s))) return rc;
+  if ((rc = launch_step(p, p->S0, p->S2, p->S2, false, first_bad, count, s))) return rc;
+  return repack(p, p->S2, p->ld, W_out, p->nl, s);
+}
+
+int cg_plan_set_step(cg_plan* p, long long step, void* stream) {
+  if (!p) return fail(CG_EINVAL, "null plan");
+  if (step < 0 || step > INT_MAX) return fail(CG_EINVAL, "step out of range");
+  set_step_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(p->step_dev, (int)step);
+  CUDA_TRY(cudaGetLastError());
+  return CG_OK;
+}
+
+struct CoupledGraph {
+  const cg_plan* bulk;
+  const cg_plan* surf;
+  double* wb;
+  double* ws;
+  int* first_bad;
+  cudaGraphExec_t chunk;
+};
+
+struct cg_coupling {
+  CouplingParams cp;
+  double* G = nullptr;  // [2][bulk] then [2][surface]
+  cudaStream_t cap_stream = nullptr, side_stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  std::vector<CoupledGraph> graphs;
+  ~cg_coupling() {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.chunk);
+    if (G) cudaFree(G);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (side_stream) cudaStreamDestroy(side_stream);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+  }
+};
+
+int cg_coupling_create(const cg_coupling_desc* d, cg_coupling** out) {
+  if (!d || !out) return fail(CG_EINVAL, "null argument");
+  *out = nullptr;
+  if (d->kind != CG_BS_BALL && d->kind != CG_BS_CYLINDER) return fail(CG_EUNSUPPORTED, "unknown coupling kind");
+  const int need = d->kind == CG_BS_BALL ? 8 : 16;
+  if (!d->params || d->nparams < need) return fail(CG_EINVAL, "coupling parameters missing");
+  for (int i = 0; i < 3; ++i)
+    if (d->nb[i] < 2) return fail(CG_EINVAL, "bulk extents must be >= 2");
+  const long long sb = d->kind == CG_BS_BALL ? (long long)d->nb[1] * d->nb[2] : (long long)d->nb[0] * d->nb[1];
+  if ((long long)d->ns[0] * d->ns[1] != sb) return fail(CG_EINVAL, "surface grid does not match the bulk trace");
+  cg_coupling* c = new cg_coupling();
+  CouplingParams& cp = c->cp;
+  cp.kind = d->kind;
+  cp.nb1 = d->nb[0];
+  cp.nb2 = d->nb[1];
+  cp.nb3 = d->nb[2];
+  cp.ns1 = d->ns[0];
+  cp.ns2 = d->ns[1];
+  cp.nbpts = (long long)d->nb[0] * d->nb[1] * d->nb[2];
+  cp.nspts = sb;
+  // caller layout (cg_coupled_kinetics); cg_coupled_run switches to the plans' storage
+  cp.ldb = cp.nb3;
+  cp.lds = cp.ns2;
+  cp.fb = cp.nbpts;
+  cp.fs = cp.nspts;
+  if (d->kind == CG_BS_BALL ? (d->ns[0] != d->nb[1] || d->ns[1] != d->nb[2])
+                            : (d->ns[0] != d->nb[0] || d->ns[1] != d->nb[1]))
+    return fail(CG_EINVAL, "surface grid does not match the bulk trace");
+  for (int i = 0; i < 16; ++i) cp.k[i] = i < d->nparams ? d->params[i] : 0.0;
+  cp.h = d->geom[0];
+  cp.rho_edge = d->geom[1];
+  for (int i = 0; i < 4; ++i) cp.lift[i] = d->lift[i];
+  auto bail = [&](cudaError_t e) {
+    delete c;
+    return fail(CG_ECUDA, std::string("cg_coupling_create: ") + cudaGetErrorString(e));
+  };
+  // reaction terms in the plans' storage layout (last axes padded to even)
+  const long long fb_s = (long long)cp.nb1 * cp.nb2 * ((cp.nb3 + 1) & ~1);
+  const long long fs_s = (long long)cp.ns1 * ((cp.ns2 + 1) & ~1);
+  cudaError_t e = cudaMalloc(&c->G, (size_t)2 * (fb_s + fs_s) * sizeof(double));
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming);
+  if (e != cudaSuccess) return bail(e);
+  *out = c;
+  return CG_OK;
+}
+
+void cg_coupling_destroy(cg_coupling* c) { delete c; }
+
+int cg_coupled_kinetics(cg_coupling* c, const double* Wb, const double* Ws, double* Gb, double* Gs, void* stream) {
+  if (!c || !Wb || !Ws || !Gb || !Gs) return fail(CG_EINVAL, "null argument");
+  CouplingParams cp = c->cp;
+  cp.Wb = Wb;
+  cp.Ws = Ws;
+  cp.Gb = Gb;
+  cp.Gs = Gs;
+  const long long total = cp.nbpts + cp.nspts;
+  coupled_kinetics_kernel<<<(unsigned)((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(cp);
+  CUDA_TRY(cudaGetLastError());
+  return CG_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// One coupled step: reaction terms from the common state, then the bulk pair
+// on stream s and the surface pair on the coupling's side stream (the two
+// step_split chains are independent once G is known), joined back on s.
+int coupled_step(cg_coupling* c, cg_plan* bulk, cg_plan* surf, const double* wb, const double* ws, double* wb_out,
+                 double* ws_out, int* first_bad, cudaStream_t s) {
+  CouplingParams cp = c->cp;
+  cp.ldb = bulk->ld;
+  cp.lds = surf->ld;
+  cp.fb = bulk->npts;
+  cp.fs = surf->npts;
+  cp.Wb = wb;
+  cp.Ws = ws;
+  cp.Gb = c->G;
+  cp.Gs = c->G + 2 * cp.fb;
+  const long long total = cp.nbpts + cp.nspts;
+  coupled_kinetics_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(cp);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(c->fork, s));
+  CUDA_TRY(cudaStreamWaitEvent(c->side_stream, c->fork, 0));
+  int rc = launch_step(surf, ws, ws_out, cp.Gs, false, first_bad + 2, true, c->side_stream);
+  if (rc) return rc;
+  if ((rc = launch_step(bulk, wb, wb_out, cp.Gb, false, first_bad, true, s))) return rc;
+  CUDA_TRY(cudaEventRecord(c->join, c->side_stream));
+  CUDA_TRY(cudaStreamWaitEvent(s, c->join, 0));
+  return CG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+static int coupled_steps(cg_coupling* c, cg_plan* bulk, cg_plan* surf, double* Wb, double* Ws, long long step0,
+                  long long nsteps, int* first_bad, cudaStream_t s);
+
+int cg_coupled_run(cg_coupling* c, cg_plan* bulk, cg_plan* surf, double* Wb, double* Ws, long long step0,
+                   long long nsteps, int* first_bad, void* stream) {
+  if (!c || !bulk || !surf || !Wb || !Ws || !first_bad) return fail(CG_EINVAL, "null argument");
   if (nsteps < 0) return fail(CG_EINVAL, "nsteps must be >= 0");
-  if (p->kin == CG_KIN_EXTERNAL) return fail(CG_EINVAL, "cg_run needs built-in kinetics");
-  if (step0 + nsteps > INT_MAX) return fail(CG_EINVAL, "step index overflow");
+  if (step0 < 0 || step0 + nsteps > INT_MAX) return fail(CG_EINVAL, "step index overflow");
+  if (bulk->B != 1 || surf->B != 1 || bulk->C != 2 || surf->C != 2)
+    return fail(CG_EINVAL, "coupled plans must hold one run of two components each");
+  if (bulk->n1 != c->cp.nb1 || bulk->n2 != c->cp.nb2 || bulk->n3 != c->cp.nb3 || surf->n1 != c->cp.ns1 ||
+      surf->n2 != c->cp.ns2)
+    return fail(CG_EINVAL, "plan grids do not match the coupling");
+  if (bulk->kin != CG_KIN_EXTERNAL || surf->kin != CG_KIN_EXTERNAL)
+    return fail(CG_EINVAL, "coupled plans must be created with CG_KIN_EXTERNAL");
+  const int want = c->cp.kind == CG_BS_BALL ? CG_BALL : CG_CYLINDER;
+  const int want_s = c->cp.kind == CG_BS_BALL ? CG_SPHERE : CG_DISK;
+  if (bulk->geom != want || surf->geom != want_s) return fail(CG_EINVAL, "plan geometries do not match the coupling");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (nsteps == 0) return CG_OK;
+  // padded plans step their storage copies (S0) of the caller's fields
+  double* wb = bulk->padded ? bulk->S0 : Wb;
+  double* ws = surf->padded ? surf->S0 : Ws;
+  int rc;
+  if (bulk->padded && (rc = repack(bulk, Wb, bulk->nl, wb, bulk->ld, s))) return rc;
+  if (surf->padded && (rc = repack(surf, Ws, surf->nl, ws, surf->ld, s))) return rc;
+  if ((rc = coupled_steps(c, bulk, surf, wb, ws, step0, nsteps, first_bad, s))) return rc;
+  if (bulk->padded && (rc = repack(bulk, wb, bulk->ld, Wb, bulk->nl, s))) return rc;
+  if (surf->padded && (rc = repack(surf, ws, surf->ld, Ws, surf->nl, s))) return rc;
+  return CG_OK;
+}
+
+static int coupled_steps(cg_coupling* c, cg_plan* bulk, cg_plan* surf, double* Wb, double* Ws, long long step0,
+                  long long nsteps, int* first_bad, cudaStream_t s) {
+  set_step_kernel<<<1, 1, 0, s>>>(bulk->step_dev, (int)step0);
+  set_step_kernel<<<1, 1, 0, s>>>(surf->step_dev, (int)step0);
+  CUDA_TRY(cudaGetLastError());
+  int rc;
+  long long done = 0;
+  if (nsteps >= kChunk) {
+    CoupledGraph* ge = nullptr;
+    for (auto& g : c->graphs)
+      if (g.bulk == bulk && g.surf == surf && g.wb == Wb && g.ws == Ws && g.first_bad == first_bad) ge = &g;
+    if (!ge) {
+      CUDA_TRY(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+      int crc = CG_OK;
+      for (int k = 0; k < kChunk && crc == CG_OK; ++k) {
+        const bool even = (k % 2) == 0;
+        crc = coupled_step(c, bulk, surf, even ? Wb : bulk->S2, even ? Ws : surf->S2, even ? bulk->S2 : Wb,
+                           even ? surf->S2 : Ws, first_bad, c->cap_stream);
+      }
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaStreamEndCapture(c->cap_stream, &graph);
+      if (crc) {
+        if (graph) cudaGraphDestroy(graph);
+        return crc;
+      }
+      if (e != cudaSuccess) return fail(CG_ECUDA, std::string("capture: ") + cudaGetErrorString(e));
+      cudaGraphExec_t exec = nullptr;
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return fail(CG_ECUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+      if (c->graphs.size() >= 4) {
+        cudaGraphExecDestroy(c->graphs.front().chunk);
+        c->graphs.erase(c->graphs.begin());
+      }
+      c->graphs.push_back(CoupledGraph{bulk, surf, Wb, Ws, first_bad, exec});
+      ge = &c->graphs.back();
+    }
+    while (nsteps - done >= kChunk) {
+      CUDA_TRY(cudaGraphLaunch(ge->chunk, s));
+      done += kChunk;
+    }
+  }
+  while (done < nsteps) {
+    if ((rc = coupled_step(c, bulk, surf, Wb, Ws, bulk->S2, surf->S2, first_bad, s))) return rc;
+    ++done;
+    if (done < nsteps) {
+      if ((rc = coupled_step(c, bulk, surf, bulk->S2, surf->S2, Wb, Ws, first_bad, s))) return rc;
+      ++done;
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(Wb, bulk->S2, (size_t)bulk->elems * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(cudaMemcpyAsync(Ws, surf->S2, (size_t)surf->elems * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  return CG_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int run_steps(cg_plan* p, double* state, long long step0, long long nsteps, int* first_bad, cudaStream_t s) {
   set_step_kernel<<<1, 1, 0, s>>>(p->step_dev, (int)step0);
   CUDA_TRY(cudaGetLastError());
   int rc;
@@ -1141,6 +1427,24 @@ int cg_run(cg_plan* p, double* state, long long step0, long long nsteps, int* fi
     }
   }
   return CG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cg_run(cg_plan* p, double* state, long long step0, long long nsteps, int* first_bad, void* stream) {
+  if (!p || !state || !first_bad) return fail(CG_EINVAL, "null argument");
+  if (nsteps < 0) return fail(CG_EINVAL, "nsteps must be >= 0");
+  if (p->kin == CG_KIN_EXTERNAL) return fail(CG_EINVAL, "cg_run needs built-in kinetics");
+  if (step0 < 0 || step0 + nsteps > INT_MAX) return fail(CG_EINVAL, "step index overflow");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (nsteps == 0) return CG_OK;
+  if (!p->padded) return run_steps(p, state, step0, nsteps, first_bad, s);
+  int rc;
+  if ((rc = repack(p, state, p->nl, p->S0, p->ld, s))) return rc;
+  if ((rc = run_steps(p, p->S0, step0, nsteps, first_bad, s))) return rc;
+  return repack(p, p->S0, p->ld, state, p->nl, s);
 }
 
 }  // extern "C"

@@ -21,7 +21,12 @@ struct StencilParams {
   int geometry;
   int n1, n2, n3;
   int ncomp, batch;
-  long long npts;  // points per field
+  long long npts;  // points per field (storage)
+  // storage layout of the F-build's input W and output F / external G: the
+  // contiguous (last) axis has logical extent n_last and row stride ldw / ldf
+  // (even, for TMA), a field holds npw / npf elements
+  int ldw, ldf;
+  long long npw, npf;
   const double* rho_b;  // [C][3][n_rho] a, b, c
   const double* phi_b;  // [C][3][n_phi]
   const double* z_b;    // [C][3][n_z]
@@ -124,7 +129,7 @@ struct FbuildShape {
 // stage component X's rows for this CTA into s[ROWS][nl]
 template <int GEOM>
 __device__ __forceinline__ void stage_rows(double* s, const double* __restrict__ X, int i0, int j, int n1, int n2,
-                                           int nl, long long rs) {
+                                           int nl, long long rs, int jst) {
   using S = FbuildShape<GEOM>;
   const bool periodic_walk = (GEOM == 1);
   const int l = threadIdx.x;
@@ -142,8 +147,8 @@ __device__ __forceinline__ void stage_rows(double* s, const double* __restrict__
 #pragma unroll
     for (int r = 0; r < S::RB; ++r) {
       const int i = min(i0 + r, n1 - 1);
-      s[(S::RB + 2 + r) * nl + l] = __ldg(X + (long long)i * rs + (long long)(jm - j) * nl + l);
-      s[(2 * S::RB + 2 + r) * nl + l] = __ldg(X + (long long)i * rs + (long long)(jp - j) * nl + l);
+      s[(S::RB + 2 + r) * nl + l] = __ldg(X + (long long)i * rs + (long long)(jm - j) * jst + l);
+      s[(2 * S::RB + 2 + r) * nl + l] = __ldg(X + (long long)i * rs + (long long)(jp - j) * jst + l);
     }
   }
 }
@@ -248,17 +253,19 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
   const int i0 = blockIdx.x * S::RB;
   const int j = S::D3 ? (int)blockIdx.y : 0;
   const int b = blockIdx.z;
-  const long long rs = S::D3 ? (long long)p.n2 * p.n3 : (long long)p.n2;
-  const long long run_base = (long long)b * p.ncomp * p.npts + (long long)j * (S::D3 ? p.n3 : 0);
+  const long long rsw = S::D3 ? (long long)p.n2 * p.ldw : (long long)p.ldw;
+  const long long rsf = S::D3 ? (long long)p.n2 * p.ldf : (long long)p.ldf;
+  const long long wbase = (long long)b * p.ncomp * p.npw + (long long)j * (S::D3 ? p.ldw : 0);
+  const long long fbase = (long long)b * p.ncomp * p.npf + (long long)j * (S::D3 ? p.ldf : 0);
   const int plane = S::ROWS * nl;
 
   if (KIN == KIN_EXTERNAL) {
     const int nc = p.ncomp < 8 ? p.ncomp : 8;
     row_coefs<GEOM>(rcs, p, i0, nc);
     for (int c = 0; c < p.ncomp; ++c) {
-      const double* X = p.W + run_base + (long long)c * p.npts;
+      const double* X = p.W + wbase + (long long)c * p.npw;
       if (c > 0) __syncthreads();
-      stage_rows<GEOM>(fb_smem, X, i0, j, n1, p.n2, nl, rs);
+      stage_rows<GEOM>(fb_smem, X, i0, j, n1, p.n2, nl, rsw, p.ldw);
       __syncthreads();
       if (l < nl) {
         const CompCoef k = comp_coef<GEOM>(p, c, l, nl);
@@ -266,7 +273,7 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
         for (int r = 0; r < S::RB; ++r) {
           const int i = i0 + r;
           if (i >= n1) break;
-          const long long idx = run_base + (long long)c * p.npts + (long long)i * rs + l;
+          const long long idx = fbase + (long long)c * p.npf + (long long)i * rsf + l;
           double val = 0.0;
           if (p.with_diffusion) val = k.coeff * diffusion_rows<GEOM>(k, rcs[(c < 8 ? c : 7) * S::RB + r], fb_smem, r, l, nl);
           if (p.with_reaction) val = p.with_diffusion ? __dadd_rn(val, __ldg(p.G + idx)) : __ldg(p.G + idx);
@@ -277,8 +284,8 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
   } else {
     const bool with_d = p.with_diffusion;
     if (with_d) row_coefs<GEOM>(rcs, p, i0, 2);
-    stage_rows<GEOM>(fb_smem, p.W + run_base, i0, j, n1, p.n2, nl, rs);
-    stage_rows<GEOM>(fb_smem + plane, p.W + run_base + p.npts, i0, j, n1, p.n2, nl, rs);
+    stage_rows<GEOM>(fb_smem, p.W + wbase, i0, j, n1, p.n2, nl, rsw, p.ldw);
+    stage_rows<GEOM>(fb_smem + plane, p.W + wbase + p.npw, i0, j, n1, p.n2, nl, rsw, p.ldw);
     CompCoef k0{}, k1{};  // operator coefficients are only present when diffusing
     if (with_d) {
       k0 = comp_coef<GEOM>(p, 0, lcl, nl);
@@ -296,7 +303,7 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
     for (int r = 0; r < S::RB; ++r) {
       const int i = i0 + r;
       if (i >= n1) break;
-      const long long off = run_base + (long long)i * rs + l;
+      const long long off = fbase + (long long)i * rsf + l;
       double g0 = 0.0, g1 = 0.0;
       if (with_r) {
         double u = fb_smem[(r + 1) * nl + l], v = fb_smem[plane + (r + 1) * nl + l];
@@ -312,7 +319,7 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
         fv = with_r ? __dadd_rn(dv, g1) : dv;
       }
       Fo[off] = fu;
-      Fo[off + p.npts] = fv;
+      Fo[off + p.npf] = fv;
     }
   }
 }

@@ -235,7 +235,7 @@ class SplitPlan:
         taus = {float(o.tau) for o in geos}
         if any(_geometry_name(o.geometry) != g or tuple(o.shape) != shape for o in geos):
             raise NotImplementedError("components of one plan must share geometry and grid "
-                                      "(mixed bulk-surface systems are out of scope)")
+                                      "(bulk-surface systems run through coupled.CoupledPlan)")
         if len(taus) != 1:
             raise ValueError("components must share tau")
         if kinetics not in KINETICS_CODES:
@@ -537,6 +537,13 @@ def run_simulation(system, m: int, t_star: float, *, record_every: int | None = 
         raise ValueError(f"unknown method {method!r}")
     if method != "split":
         raise NotImplementedError("forward Euler is a reference comparison path, not part of the engine")
+    from .models import BulkSurfaceCoupling
+
+    if isinstance(getattr(system, "kinetics", None), BulkSurfaceCoupling):
+        from .coupled import run_coupled
+
+        return run_coupled(system, m, t_star, record_every=record_every, diagnostics=diagnostics,
+                           sample_hook=sample_hook, as_torch=as_torch)
     kin = engine_kinetics(system)
     tau = t_star / m
     comps = list(system.components)

@@ -7,8 +7,10 @@ libcurvigpu.so), ``SystemComponent``, ``CoupledSystem``, ``model_spec``,
 ``build_system``, ``random_initial_condition``.  The reference's kinetics are
 arbitrary Python closures (models.py:386-391); the engine instead takes a
 :class:`Kinetics` descriptor naming one of the pointwise reactions compiled
-into the F-build kernel.  Bulk-surface models (models.py:322-369, :570-661)
-are out of scope (SURVEY 8(f) "next") and raise NotImplementedError.
+into the F-build kernel.  The two bulk-surface models (models.py:322-369,
+:570-661) carry a :class:`BulkSurfaceCoupling` descriptor instead, evaluated
+by the coupling kernel (csrc/coupling.cuh) inside the coupled time loop
+(paper_2604_11558_b200/coupled.py).
 """
 
 from __future__ import annotations
@@ -22,7 +24,7 @@ import numpy as np
 
 from . import _native
 from .integrators import ComponentOps, Geometry
-from .operators import DiagonalWeights, build_lambda, build_phi_op, build_rho, build_theta
+from .operators import DiagonalWeights, build_lambda, build_phi_op, build_rho, build_theta, build_z
 
 # ---------------------------------------------------------------------------
 # seeded random numbers (models.py:43-130), C-backed
@@ -129,6 +131,42 @@ class Kinetics:
         return np.array([float(self.params[k]) for k in KINETICS_PARAMS[self.kind]])
 
 
+BULK_SURFACE_PARAMS = {
+    "ball": ("alpha1", "alpha2", "beta1", "zeta1", "zeta2", "zeta3", "eta1", "eta2"),
+    "cylinder": ("alpha1", "alpha2", "alpha3", "beta1", "beta2", "beta3", "delta",
+                 "zeta1", "zeta2", "zeta3", "zeta4", "zeta5", "eta1", "eta2", "eta3", "eta5"),
+}
+
+
+@dataclass(frozen=True)
+class BulkSurfaceCoupling:
+    """Reaction terms of a four-component bulk-surface system (bulk u, v;
+    surface r, s), evaluated on the GPU from the common state:
+
+    - ``ball``: alpha1 * Schnakenberg in the bulk plus the Robin ghost sources
+      on the outermost rho slice, surface zeta1 * (Schnakenberg - exchange)
+      (models.py:322-345, :587-602); ``h`` = h_rho, ``rho_edge`` = last rho node
+    - ``cylinder``: linear bulk relaxation plus the flux sources on the z = 0
+      slice, surface zeta1 * DIB with the v-dependent deposition term
+      (models.py:348-369, :633-649); ``h`` = h_z
+    """
+
+    kind: str
+    params: dict
+    h: float
+    rho_edge: float = 0.0
+
+    def __post_init__(self):
+        if self.kind not in BULK_SURFACE_PARAMS:
+            raise NotImplementedError(f"no bulk-surface coupling {self.kind!r}")
+        missing = [k for k in BULK_SURFACE_PARAMS[self.kind] if k not in self.params]
+        if missing:
+            raise ValueError(f"{self.kind} coupling missing parameters {missing}")
+
+    def param_vector(self) -> np.ndarray:
+        return np.array([float(self.params[k]) for k in BULK_SURFACE_PARAMS[self.kind]])
+
+
 # ---------------------------------------------------------------------------
 # systems
 # ---------------------------------------------------------------------------
@@ -147,7 +185,8 @@ class SystemComponent:
 
 @dataclass(frozen=True)
 class CoupledSystem:
-    """models.py:386-396, with ``kinetics`` a :class:`Kinetics` descriptor."""
+    """models.py:386-396, with ``kinetics`` a :class:`Kinetics` (or, for the
+    bulk-surface models, :class:`BulkSurfaceCoupling`) descriptor."""
 
     spec: object
     components: list
@@ -167,7 +206,7 @@ class ModelName(Enum):
     BSDIB_CYLINDER = "bsdib_cylinder"
 
 
-# published defaults of the three single-geometry models (models.py:148-178)
+# published defaults (models.py:148-221)
 _DEFAULTS = {
     ModelName.BVAM_DISK: ({"gamma": 3.87e-3, "delta": 7.5e-3, "alpha1": 0.899, "alpha2": 0.2,
                            "alpha3": 0.2, "beta1": -0.91, "beta2": -0.899}, {"rho_star": 1.0}),
@@ -176,6 +215,14 @@ _DEFAULTS = {
     ModelName.DIB_SPHERE: ({"zeta1": 10.0, "zeta2": 10.0, "zeta3": 1.0, "zeta4": 48.0, "zeta5": 0.5,
                             "eta1": 5.0, "eta2": 2.5, "eta3": 0.2, "eta5": 1.5, "epsilon": 20.0},
                            {"rho_star": 1.1653}),
+    ModelName.BULK_SURFACE_SCHNAKENBERG_BALL: ({"alpha1": 55.0, "alpha2": 0.1, "beta1": 0.9, "zeta1": 55.0,
+                                                "zeta2": 5.0 / 12.0, "zeta3": 5.0 / 12.0, "eta1": 5.0,
+                                                "eta2": 5.0, "delta": 10.0, "epsilon": 10.0},
+                                               {"rho_star": 1.0}),
+    ModelName.BSDIB_CYLINDER: ({"alpha1": 1.0, "alpha2": 1.0, "alpha3": 0.15, "beta1": 1.0, "beta2": 1.0,
+                                "beta3": 0.15, "delta": 1.0, "epsilon": 20.0, "zeta1": 1.0, "zeta2": 10.0,
+                                "zeta3": 1.0, "zeta4": 66.0, "zeta5": 0.5, "eta1": 3.0, "eta2": 2.5,
+                                "eta3": 0.2, "eta5": 1.5}, {"rho_star": 25.0, "z_star": 25.0}),
 }
 
 
@@ -195,14 +242,16 @@ class ModelSpec:
             return {"u": ue, "v": p["beta1"] / ue**2}
         if self.name is ModelName.DIB_SPHERE:
             return {"r": 0.0, "s": p["zeta5"]}
-        raise NotImplementedError(f"{self.name.value} is a bulk-surface model (out of scope)")
+        if self.name is ModelName.BULK_SURFACE_SCHNAKENBERG_BALL:
+            ue = p["alpha2"] + p["beta1"]
+            ve = p["beta1"] / ue**2
+            return {"u": ue, "v": ve, "r": ue, "s": ve}
+        return {"u": p["alpha2"], "v": p["beta2"], "r": 0.0, "s": p["zeta5"]}
 
 
 def model_spec(name, overrides=None) -> ModelSpec:
-    """models.py:247-276 for the single-geometry models."""
+    """models.py:247-276."""
     name = ModelName(name) if isinstance(name, str) else name
-    if name not in _DEFAULTS:
-        raise NotImplementedError(f"{name.value} is a bulk-surface model (out of scope, SURVEY 8(f))")
     params, sizes = (dict(x) for x in _DEFAULTS[name])
     for key, value in (overrides or {}).items():
         if key in sizes:
@@ -215,22 +264,41 @@ def model_spec(name, overrides=None) -> ModelSpec:
         perts = {"u": Uniform(-0.5, 0.5), "v": Uniform(-0.5, 0.5)}
     elif name is ModelName.SCHNAKENBERG_ANOMALOUS_DISK:
         perts = {"u": Normal(1e-5), "v": Normal(1e-5)}
-    else:
+    elif name is ModelName.DIB_SPHERE:
         perts = {"r": Normal(1e-6), "s": Normal(1e-6)}
+    elif name is ModelName.BULK_SURFACE_SCHNAKENBERG_BALL:
+        perts = {c: Normal(1e-3) for c in ("u", "v", "r", "s")}
+    else:
+        perts = {"u": None, "v": None, "r": Uniform(0.0, 1e-2), "s": Uniform(0.0, 1e-2)}
     return ModelSpec(name, params, sizes, perts)
+
+
+def component_shapes(name, dims: dict) -> dict:
+    """Field dims per component (models.py:435-451)."""
+    name = ModelName(name) if isinstance(name, str) else name
+    if name in (ModelName.BVAM_DISK, ModelName.SCHNAKENBERG_ANOMALOUS_DISK):
+        shape = (dims["n_rho"], dims["n_theta"])
+        return {"u": shape, "v": shape}
+    if name is ModelName.DIB_SPHERE:
+        shape = (dims["n_theta"], dims["n_phi"])
+        return {"r": shape, "s": shape}
+    if name is ModelName.BULK_SURFACE_SCHNAKENBERG_BALL:
+        bulk = (dims["n_rho"], dims["n_theta"], dims["n_phi"])
+        surf = (dims["n_theta"], dims["n_phi"])
+    else:
+        bulk = (dims["n_rho"], dims["n_theta"], dims["n_z"])
+        surf = (dims["n_rho"], dims["n_theta"])
+    return {"u": bulk, "v": bulk, "r": surf, "s": surf}
 
 
 def random_initial_condition(spec: ModelSpec, seed: int, dims: dict) -> dict:
     """Equilibrium + seeded perturbation, one generator, component-major, F
     order (models.py:412-432)."""
     rng = Xoshiro256pp(seed)
-    if spec.name is ModelName.DIB_SPHERE:
-        shape = (dims["n_theta"], dims["n_phi"])
-    else:
-        shape = (dims["n_rho"], dims["n_theta"])
+    shapes = component_shapes(spec.name, dims)
     eq = spec.equilibrium()
     out = {}
-    for name in eq:
+    for name, shape in shapes.items():
         base = np.full(shape, eq[name])
         law = spec.perturbations[name]
         if law is not None:
@@ -244,8 +312,8 @@ def _component(spec, name, ops, init, lift=0.0):
 
 
 def build_system(spec, dims: dict, seed: int, overrides=None) -> CoupledSystem:
-    """models.py:454-472 for bvam_disk, schnakenberg_anomalous_disk and
-    dib_sphere, with GPU kinetics descriptors instead of closures."""
+    """models.py:454-472 (builders :475-661), with GPU kinetics / coupling
+    descriptors instead of closures."""
     if not isinstance(spec, ModelSpec):
         spec = model_spec(spec, overrides)
     elif overrides:
@@ -268,7 +336,7 @@ def build_system(spec, dims: dict, seed: int, overrides=None) -> CoupledSystem:
         comps = [_component(spec, "u", make(1.0), init, eq["u"]),
                  _component(spec, "v", make(p["delta"]), init, eq["v"])]
         kin = Kinetics("schnakenberg", {"gamma": p["alpha1"], "a": p["alpha2"], "b": p["beta1"]})
-    else:
+    elif spec.name is ModelName.DIB_SPHERE:
         rs = spec.sizes["rho_star"]
         theta = build_theta(dims["n_theta"])
         phi, _ = build_phi_op(dims["n_phi"])
@@ -276,4 +344,28 @@ def build_system(spec, dims: dict, seed: int, overrides=None) -> CoupledSystem:
         comps = [_component(spec, "r", make(1.0 / rs**2), init),
                  _component(spec, "s", make(p["epsilon"] / rs**2), init)]
         kin = Kinetics("dib", {k: p[k] for k in KINETICS_PARAMS["dib"]})
+    elif spec.name is ModelName.BULK_SURFACE_SCHNAKENBERG_BALL:
+        # models.py:570-611
+        rs = spec.sizes["rho_star"]
+        rho = build_rho(3, dims["n_rho"], rs)
+        theta = build_theta(dims["n_theta"])
+        phi, _ = build_phi_op(dims["n_phi"])
+        bulk = lambda k: ComponentOps(Geometry.BALL, k, rho=rho, theta=theta, phi=phi)  # noqa: E731
+        surf = lambda k: ComponentOps(Geometry.SPHERE, k, theta=theta, phi=phi)  # noqa: E731
+        comps = [_component(spec, "u", bulk(1.0), init), _component(spec, "v", bulk(p["delta"]), init),
+                 _component(spec, "r", surf(1.0 / rs**2), init),
+                 _component(spec, "s", surf(p["epsilon"] / rs**2), init)]
+        kin = BulkSurfaceCoupling("ball", {k: p[k] for k in BULK_SURFACE_PARAMS["ball"]},
+                                  h=float(rho.h), rho_edge=float(rho.grid[-1]))
+    else:
+        # models.py:614-661
+        rho = build_rho(2, dims["n_rho"], spec.sizes["rho_star"])
+        theta = build_theta(dims["n_theta"])
+        z = build_z(dims["n_z"], spec.sizes["z_star"])
+        bulk = lambda k: ComponentOps(Geometry.CYLINDER, k, rho=rho, theta=theta, z=z)  # noqa: E731
+        surf = lambda k: ComponentOps(Geometry.DISK, k, rho=rho, theta=theta)  # noqa: E731
+        comps = [_component(spec, "u", bulk(1.0), init, eq["u"]),
+                 _component(spec, "v", bulk(p["delta"]), init, eq["v"]),
+                 _component(spec, "r", surf(1.0), init), _component(spec, "s", surf(p["epsilon"]), init)]
+        kin = BulkSurfaceCoupling("cylinder", {k: p[k] for k in BULK_SURFACE_PARAMS["cylinder"]}, h=float(z.h))
     return CoupledSystem(spec=spec, components=comps, kinetics=kin, equilibrium=eq)

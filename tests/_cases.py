@@ -18,6 +18,14 @@ CASES = [
     "ball_12x10x18",
     "cylinder_9x20x24",
     "cylinderD_6x8x10",
+    # odd contiguous (last) axes: the reference's own test bases
+    # (tests/test_integrators.py:38 ball_base(3, 4, 3); tests/test_models.py:183
+    # dib_sphere (8, 5)) and odd theta on the disk
+    "ball_3x4x3",
+    "sphere_8x5",
+    "disk_5x7",
+    "cylinder_3x4x5",
+    "sphere_7x9",
 ]
 
 
@@ -49,6 +57,18 @@ def engine_base(name):
     if name == "cylinderD_6x8x10":
         return ComponentOps(Geometry.CYLINDER, 0.3, rho=op.build_rho(2, 6, 1.0), theta=op.build_theta(8),
                             z=op.build_z(10, 1.5))
+    if name == "ball_3x4x3":
+        return ComponentOps(Geometry.BALL, 1.1, rho=op.build_rho(3, 3, 1.0), theta=op.build_theta(4),
+                            phi=op.build_phi_op(3)[0])
+    if name == "sphere_8x5":
+        return ComponentOps(Geometry.SPHERE, 0.9, theta=op.build_theta(8), phi=op.build_phi_op(5)[0])
+    if name == "disk_5x7":
+        return ComponentOps(Geometry.DISK, 0.7, rho=op.build_rho(2, 5, 1.0), theta=op.build_theta(7))
+    if name == "cylinder_3x4x5":
+        return ComponentOps(Geometry.CYLINDER, 0.8, rho=op.build_rho(2, 3, 1.0), theta=op.build_theta(4),
+                            z=op.build_z(5, 1.0))
+    if name == "sphere_7x9":
+        return ComponentOps(Geometry.SPHERE, 0.3, theta=op.build_theta(7), phi=op.build_phi_op(9)[0])
     raise KeyError(name)
 
 
@@ -80,4 +100,16 @@ def oracle_comp(name):
     if name == "cylinderD_6x8x10":
         return orc.Comp("w", "cylinder", 0.3, rho=orc.radial_stencil(2, 6, 1.0), theta=orc.theta_stencil(8),
                         z=orc.axial_stencil_nd(10, 1.5))
+    if name == "ball_3x4x3":
+        return orc.Comp("w", "ball", 1.1, rho=orc.radial_stencil(3, 3, 1.0), theta=orc.theta_stencil(4),
+                        phi=orc.polar_stencil(3))
+    if name == "sphere_8x5":
+        return orc.Comp("w", "sphere", 0.9, theta=orc.theta_stencil(8), phi=orc.polar_stencil(5))
+    if name == "disk_5x7":
+        return orc.Comp("w", "disk", 0.7, rho=orc.radial_stencil(2, 5, 1.0), theta=orc.theta_stencil(7))
+    if name == "cylinder_3x4x5":
+        return orc.Comp("w", "cylinder", 0.8, rho=orc.radial_stencil(2, 3, 1.0), theta=orc.theta_stencil(4),
+                        z=orc.axial_stencil_nd(5, 1.0))
+    if name == "sphere_7x9":
+        return orc.Comp("w", "sphere", 0.3, theta=orc.theta_stencil(7), phi=orc.polar_stencil(9))
     raise KeyError(name)

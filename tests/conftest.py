@@ -42,6 +42,7 @@ def golden():
         steps = dict(np.load(GOLDEN / "steps.npz"))
         runs = dict(np.load(GOLDEN / "runs.npz"))
         full = dict(np.load(GOLDEN / "full.npz")) if (GOLDEN / "full.npz").exists() else {}
+        bs = dict(np.load(GOLDEN / "bulk_surface.npz"))
 
     return G
 

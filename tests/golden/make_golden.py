@@ -13,6 +13,10 @@ Outputs (committed; small):
   full.npz         the five BASELINE configs at FULL size: IC checksums and
                    strided samples / norms of the physical fields after
                    step 1 and step 100 (config 5: members 0, 255, 511)
+  bulk_surface.npz the two bulk-surface models (models.py:570-661) through
+                   model_spec/build_system/run_simulation: small grids in
+                   full (IC, kinetics at the IC, state after 20 steps) and
+                   the paper's full-size grids (samples after 1 and 100 steps)
 
 The BASELINE systems are built through the reference's public API exactly as
 SURVEY.md Appendix A prescribes (custom kinetics closures for configs 1-4,
@@ -231,6 +235,13 @@ def _bases():
                                          theta=op.build_theta(20), z=z_neumann(24, 2.0)),
         "cylinderD_6x8x10": ComponentOps(Geometry.CYLINDER, 0.3, rho=op.build_rho(2, 6, 1.0),
                                          theta=op.build_theta(8), z=op.build_z(10, 1.5)),
+        "ball_3x4x3": ComponentOps(Geometry.BALL, 1.1, rho=op.build_rho(3, 3, 1.0), theta=op.build_theta(4),
+                                   phi=op.build_phi_op(3)[0]),
+        "sphere_8x5": ComponentOps(Geometry.SPHERE, 0.9, theta=op.build_theta(8), phi=op.build_phi_op(5)[0]),
+        "disk_5x7": ComponentOps(Geometry.DISK, 0.7, rho=op.build_rho(2, 5, 1.0), theta=op.build_theta(7)),
+        "cylinder_3x4x5": ComponentOps(Geometry.CYLINDER, 0.8, rho=op.build_rho(2, 3, 1.0),
+                                       theta=op.build_theta(4), z=op.build_z(5, 1.0)),
+        "sphere_7x9": ComponentOps(Geometry.SPHERE, 0.3, theta=op.build_theta(7), phi=op.build_phi_op(9)[0]),
     }
 
 
@@ -314,8 +325,58 @@ def make_full():
     np.savez_compressed(HERE / "full.npz", **d)
 
 
+BS_CASES = {
+    # name: (model, dims, m, t_star, seed, overrides)
+    "ball_s": ("bulk_surface_schnakenberg_ball", {"n_rho": 6, "n_theta": 8, "n_phi": 6}, 20, 20 * 1e-4, 1, None),
+    "ball_odd": ("bulk_surface_schnakenberg_ball", {"n_rho": 5, "n_theta": 10, "n_phi": 7}, 20, 20 * 1e-4, 3, None),
+    "ball_zero": ("bulk_surface_schnakenberg_ball", {"n_rho": 4, "n_theta": 6, "n_phi": 4}, 20, 0.002, 9,
+                  {"zeta2": 0.0, "zeta3": 0.0, "eta1": 0.0, "eta2": 0.0}),
+    "cyl_s": ("bsdib_cylinder", {"n_rho": 6, "n_theta": 8, "n_z": 5}, 20, 20 * 6.25e-3, 1, None),
+    "cyl_odd": ("bsdib_cylinder", {"n_rho": 7, "n_theta": 12, "n_z": 4}, 20, 20 * 6.25e-3, 4, None),
+    # the paper's full-size runs (pkg/configs/ball_full.cfg, cylinder_full.cfg), 1 and 100 steps
+    "ball_full": ("bulk_surface_schnakenberg_ball", {"n_rho": 30, "n_theta": 50, "n_phi": 30}, 100, 100 * 1e-4,
+                  1, None),
+    "cyl_full": ("bsdib_cylinder", {"n_rho": 160, "n_theta": 160, "n_z": 20}, 100, 100 * 6.25e-3, 1, None),
+}
+
+
+def make_bulk_surface():
+    """bulk_surface.npz: the two bulk-surface models through the reference's
+    own model_spec/build_system/run_simulation.  Small cases keep the whole
+    fields (IC, kinetics at the IC, state after m steps); the full-size cases
+    keep IC checksums and strided samples after 1 and m steps."""
+    d = {}
+    for key, (name, dims, m, t_star, seed, over) in BS_CASES.items():
+        t0 = time.time()
+        spec = models.model_spec(name, over)
+        sysm = models.build_system(spec, dims, seed)
+        full = key.endswith("_full")
+        states0 = {c.name: c.initial for c in sysm.components}
+        g0 = sysm.kinetics({k: v.copy() for k, v in states0.items()})
+        for c in sysm.components:
+            if full:
+                d[f"{key}_{c.name}_init_sum"] = np.array(np.sum(c.initial))
+                d[f"{key}_{c.name}_init_sample"] = c.initial.ravel()[_sample_idx(c.initial.size)]
+            else:
+                d[f"{key}_{c.name}_init"] = c.initial
+                d[f"{key}_{c.name}_g0"] = g0[c.name]
+        d[f"{key}_m"] = np.array(m)
+        d[f"{key}_t"] = np.array(t_star)
+        if full:
+            r1 = run_simulation(sysm, 1, t_star / m)
+            _record(d, f"{key}_s1", sysm, r1.fields)
+            rm = run_simulation(sysm, m, t_star)
+            _record(d, f"{key}_s{m}", sysm, rm.fields)
+        else:
+            res = run_simulation(sysm, m, t_star)
+            for c in sysm.components:
+                d[f"{key}_{c.name}_final"] = res.fields[c.name]
+        print(f"{key}: {time.time() - t0:.1f}s", flush=True)
+    np.savez_compressed(HERE / "bulk_surface.npz", **d)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "setup", "steps", "runs", "full"]
+    which = sys.argv[1:] or ["rng", "setup", "steps", "runs", "full", "bulk_surface"]
     for w in which:
         t0 = time.time()
         globals()[f"make_{w}"]()

@@ -136,6 +136,28 @@ def test_kinetics_descriptor_validation():
     assert np.array_equal(k.param_vector(), [0.04, 0.06])
 
 
-def test_bulk_surface_models_are_out_of_scope():
+@pytest.mark.parametrize("key,name,dims", [
+    ("ball_s", "bulk_surface_schnakenberg_ball", {"n_rho": 6, "n_theta": 8, "n_phi": 6}),
+    ("cyl_s", "bsdib_cylinder", {"n_rho": 6, "n_theta": 8, "n_z": 5}),
+])
+def test_bulk_surface_systems_match_reference(golden, key, name, dims):
+    """build_system of the bulk-surface models: seeded ICs bitwise, lifts,
+    shapes and the coupling descriptor (models.py:570-661)."""
+    sysm = models.build_system(name, dims, 1)
+    assert [c.name for c in sysm.components] == ["u", "v", "r", "s"]
+    for c in sysm.components:
+        np.testing.assert_array_equal(c.initial, golden.bs[f"{key}_{c.name}_init"])
+    kin = sysm.kinetics
+    assert isinstance(kin, models.BulkSurfaceCoupling)
+    if kin.kind == "ball":
+        assert [c.lift for c in sysm.components] == [0.0] * 4
+        assert kin.rho_edge == 1.0 and kin.h > 0
+        assert len(kin.param_vector()) == 8
+    else:
+        assert [c.lift for c in sysm.components] == [1.0, 1.0, 0.0, 0.0]
+        assert kin.h == 25.0 / 5
+        assert len(kin.param_vector()) == 16
+    with pytest.raises(ValueError):
+        models.BulkSurfaceCoupling("ball", {"alpha1": 1.0}, h=0.1)
     with pytest.raises(NotImplementedError):
-        models.model_spec("bulk_surface_schnakenberg_ball")
+        models.BulkSurfaceCoupling("torus", {}, h=0.1)

@@ -42,8 +42,8 @@ def test_plan_create_rejects_bad_descriptors_without_touching_the_gpu():
     assert rc == _native.CG_EINVAL
     assert b"geometry" in lib.cg_last_error()
     d.geometry = 0
-    d.n[0], d.n[1], d.n[2] = 64, 127, 1  # odd contiguous axis is unsupported
-    d.batch, d.ncomp = 1, 2
+    d.n[0], d.n[1], d.n[2] = 64, 127, 1
+    d.batch, d.ncomp = 1, 3  # built-in kinetics are two-species
     d.kinetics = 1
     rc = lib.cg_plan_create(ctypes.byref(d), ctypes.byref(h))
     assert rc == _native.CG_EUNSUPPORTED
