@@ -265,6 +265,69 @@ def per_config_gpu(k, steps=200, warmup=20, theta=None):
             "step_frac_fp64_peak": flops / sec / 1e12 / FP64_PEAK_TFLOPS}
 
 
+BULK_SURFACE = {
+    # the paper's full-size bulk-surface runs (pkg/configs/ball_full.cfg, cylinder_full.cfg)
+    "ball_full": ("bulk_surface_schnakenberg_ball", {"n_rho": 30, "n_theta": 50, "n_phi": 30}, 200000, 20.0),
+    "cylinder_full": ("bsdib_cylinder", {"n_rho": 160, "n_theta": 160, "n_z": 20}, 8000, 50.0),
+}
+
+
+def bulk_surface_gpu(key, steps=320, warmup=32):
+    """One-GPU throughput of a full-size bulk-surface model: one coupled step
+    = coupling kernel + bulk step_split + surface step_split (cg_coupled_run,
+    graph-replayed)."""
+    import numpy as np
+    import torch
+
+    from paper_2604_11558_b200 import models
+    from paper_2604_11558_b200.coupled import CoupledPlan
+    from paper_2604_11558_b200.integrators import prepare
+
+    name, dims, m, t_star = BULK_SURFACE[key]
+    system = models.build_system(name, dims, 1)
+    tau = t_star / m
+    comps = system.components
+    plan = CoupledPlan([prepare(c.ops, tau) for c in comps], system.kinetics, lifts=[c.lift for c in comps])
+    plan.load([c.initial for c in comps])
+    plan.run(0, warmup)
+    plan.load([c.initial for c in comps])
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    plan.run(0, steps)
+    e1.record()
+    e1.synchronize()
+    sec = e0.elapsed_time(e1) / 1e3 / steps
+    dof = sum(int(np.prod(c.ops.shape)) for c in comps)
+    ok = bool((plan.first_bad.cpu().numpy() == 2**31 - 1).all())
+    plan.close()
+    return {"model": name, "dims": dims, "dof": dof, "ms_per_step": sec * 1e3, "dof_steps_per_s": dof / sec,
+            "paper_run_s": sec * m, "paper_steps": m, "no_divergence": ok}
+
+
+def bulk_surface_cpu(key, steps=3):
+    """The same step through the oracle port on the host (BLAS threads as set)."""
+    import time
+
+    from oracle import configs as ocfg
+    from oracle import curvi_oracle as orc
+    from paper_2604_11558_b200 import models
+
+    name, dims, m, t_star = BULK_SURFACE[key]
+    system = models.build_system(name, dims, 1)
+    init = [c.initial for c in system.components]
+    d = tuple(dims.values())
+    osys = ocfg.bs_ball(d, initial=init) if key.startswith("ball") else ocfg.bs_cylinder(d, initial=init)
+    tau = t_star / m
+    orc.integrate(osys, 1, tau)
+    t0 = time.perf_counter()
+    orc.integrate(osys, steps, steps * tau)
+    sec = (time.perf_counter() - t0) / steps
+    dof = sum(int(c.initial.size) for c in system.components)
+    return {"model": name, "ms_per_step": sec * 1e3, "dof_steps_per_s": dof / sec, "kind": "port",
+            "threads": os.environ.get("OPENBLAS_NUM_THREADS", "default (all cores)")}
+
+
 def engine_arm(args):
     import numpy as np
     import torch
@@ -391,6 +454,8 @@ def engine_arm(args):
         line["per_config"] = [per_config_gpu(k, theta=t) for k in (1, 2, 3, 4) for t in ("fft", "gemm")]
         line["variants"] = theta_variants(ens, init_dev, chunk, stream)
         line["per_config_cpu"] = cpu_per_config()
+        line["bulk_surface"] = [bulk_surface_gpu(k) for k in BULK_SURFACE]
+        line["bulk_surface_cpu"] = [bulk_surface_cpu(k) for k in BULK_SURFACE]
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

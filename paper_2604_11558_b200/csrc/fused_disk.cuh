@@ -1,12 +1,17 @@
-// Disk front end fused into one pass: F-build (stencil diffusion + kinetics)
-// and the FFT theta propagator, W -> T = Q(Phi o Q^T F) row by row.
+// Disk front end fused into one persistent pass: F-build (stencil diffusion +
+// kinetics) and the FFT theta propagator, W -> T = Q(Phi o Q^T F) row by row.
 //
-// For the disk the theta axis is the contiguous one, so a CTA that owns RPB
-// consecutive rho rows of BOTH species of one run can stage W_u, W_v rows
-// i0-1 .. i0+RPB in shared memory, evaluate F for its rows on the fly inside
-// forward FFT phase A (F is never written to HBM), and run the rest of the
-// propagator (thetafft.cuh theta_tail).  HBM traffic per step drops from
-// read W + write F + read F + write T to read W + write T.
+// For the disk the theta axis is the contiguous one, so a work item = RPB
+// consecutive rho rows of BOTH species of one run (LPB = 2 RPB FFT lines).
+// Its W rows i0-1 .. i0+RPB (both species) and its Phi rows arrive by 1-D
+// bulk copies into one of two shared-memory buffers; the CTA evaluates F for
+// its lines on the fly inside forward FFT phase A (F never goes to HBM) and
+// runs the rest of the propagator (thetafft.cuh theta_tail) with Phi and the
+// twiddles read from shared memory.  One CTA per SM walks the items
+// persistently; item t+2's copies are issued as soon as item t has released
+// its buffer, so HBM reads stay in flight under the FFT arithmetic.
+// HBM traffic per step: read W (+2 halo rows per RPB) + write T, instead of
+// read W + write F + read F + write T for fbuild_rows + theta_fast.
 #pragma once
 
 #include "stencil.cuh"
@@ -17,85 +22,142 @@ namespace cg {
 template <int M1, int M2>
 struct FusedDisk {
   using F = FastTheta<M1, M2>;
-  static constexpr int RPB = F::LPB / 2;  // rho rows per CTA (lines = 2 species x RPB rows)
-  static constexpr int N = 2 * F::M;      // theta extent
-  static constexpr size_t stage_bytes = (size_t)2 * (RPB + 2) * N * sizeof(double);
-  static constexpr size_t smem = F::smem + stage_bytes;
+  static constexpr int M = F::M;
+  static constexpr int N = 2 * M;         // theta extent
+  static constexpr int LPB = F::LPB;      // FFT lines per item
+  static constexpr int RPB = LPB / 2;     // rho rows per item (2 species)
+  static constexpr size_t wst = (size_t)2 * (RPB + 2) * N * sizeof(double);   // staged W rows
+  static constexpr size_t sft = (size_t)LPB * F::SL * sizeof(double2);        // FFT tile (overlays W)
+  static constexpr size_t reg_a = ((wst > sft ? wst : sft) + 127) / 128 * 128;
+  static constexpr size_t phib = (size_t)LPB * (M + 1) * sizeof(double);     // Phi rows of the item
+  static constexpr size_t buf = reg_a + (phib + 127) / 128 * 128;
+  static constexpr size_t twb = (size_t)N * sizeof(double2);
+  static constexpr size_t smem = 128 + twb + 2 * buf + 64;                    // + alignment slack, barriers
+  static_assert(RPB % 2 == 0, "Phi row blocks must stay 16-byte aligned");
 };
 
 template <int M1, int M2, int KIN>
-__global__ void __launch_bounds__(256) disk_ftheta_kernel(const ThetaParams tp, const StencilParams sp) {
+__global__ void __launch_bounds__(256, 1) disk_ftheta_kernel(const ThetaParams tp, const StencilParams sp) {
   using F = FastTheta<M1, M2>;
   using D = FusedDisk<M1, M2>;
   constexpr int M = F::M, TPL = F::TPL, RPB = D::RPB, N = D::N;
-  extern __shared__ double2 fd_smem[];
-  double2* Sbase = fd_smem;
-  double* Wst = reinterpret_cast<double*>(fd_smem + F::LPB * F::SL);  // [2][RPB+2][N]
+  extern __shared__ uint8_t fd_raw[];
+  uint8_t* base_s = fd_raw + ((128u - (smem_u32(fd_raw) & 127u)) & 127u);  // stays a shared-space pointer
+  double2* tw_s = reinterpret_cast<double2*>(base_s);
+  uint8_t* bufs = base_s + D::twb;
+  uint64_t* full = reinterpret_cast<uint64_t*>(bufs + 2 * D::buf);  // [2] item buffers, [2] twiddles
 
-  if (sp.step && blockIdx.x == 0 && threadIdx.x == 0) *sp.step += 1;
   const int n1 = sp.n1;
   const int per = n1 / RPB;
-  const int b = blockIdx.x / per;
-  const int i0 = (blockIdx.x - b * per) * RPB;
-  const long long run = (long long)b * 2 * sp.npts;
+  const int items = sp.batch * per;
+  const long long fsz = sp.npts;  // disk plans are never padded here
+  const uint32_t row_bytes = N * sizeof(double);
+  const uint32_t item_bytes = (uint32_t)(2 * (RPB + 2) * row_bytes + 2 * RPB * (M + 1) * sizeof(double));
 
-  // ---- stage W_u, W_v rows i0-1 .. i0+RPB (clamped rows are never used by the stencil)
-  for (int idx = threadIdx.x; idx < 2 * (RPB + 2) * (N / 2); idx += blockDim.x) {
-    const int comp = idx / ((RPB + 2) * (N / 2));
-    const int rem = idx - comp * (RPB + 2) * (N / 2);
-    const int r = rem / (N / 2), k = rem - r * (N / 2);
-    const int i = min(max(i0 - 1 + r, 0), n1 - 1);
-    const double2 v =
-        __ldg(reinterpret_cast<const double2*>(sp.W + run + (long long)comp * sp.npts + (long long)i * N) + k);
-    reinterpret_cast<double2*>(Wst + (comp * (RPB + 2) + r) * N)[k] = v;
+  if (sp.step && blockIdx.x == 0 && threadIdx.x == 0) *sp.step += 1;
+
+  // copies of one item into buffer k (issued by one thread)
+  auto issue = [&](int item, int k) {
+    const int b = item / per;
+    const int i0 = (item - b * per) * RPB;
+    uint8_t* bb = bufs + k * D::buf;
+    double* wst = reinterpret_cast<double*>(bb);
+    double* phs = reinterpret_cast<double*>(bb + D::reg_a);
+    mbar_arrive_expect_tx(&full[k], item_bytes);
+    const int lo = i0 > 0 ? i0 - 1 : 0;
+    const int hi = (i0 + RPB < n1) ? i0 + RPB : n1 - 1;
+    for (int comp = 0; comp < 2; ++comp) {
+      const double* src = sp.W + ((long long)b * 2 + comp) * fsz;
+      double* dst = wst + (size_t)comp * (RPB + 2) * N;
+      // staging row r <-> rho row i0 - 1 + r; missing halo rows are clamped
+      // copies (their stencil coefficient is zero, they only need to be finite)
+      bulk_load_1d(dst + (size_t)(lo - (i0 - 1)) * N, src + (long long)lo * N, (uint32_t)(hi - lo + 1) * row_bytes,
+                   &full[k]);
+      if (i0 == 0) bulk_load_1d(dst, src, row_bytes, &full[k]);
+      if (i0 + RPB >= n1) bulk_load_1d(dst + (size_t)(RPB + 1) * N, src + (long long)(n1 - 1) * N, row_bytes, &full[k]);
+      bulk_load_1d(phs + (size_t)comp * RPB * (M + 1), tp.phif + ((long long)comp * tp.nclass + i0) * (M + 1),
+                   (uint32_t)(RPB * (M + 1) * sizeof(double)), &full[k]);
+    }
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&full[2], 1);
+    fence_barrier_init();
   }
   __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&full[2], (uint32_t)D::twb);
+    bulk_load_1d(tw_s, tp.tw, (uint32_t)D::twb, &full[2]);
+    if ((int)blockIdx.x < items) issue(blockIdx.x, 0);
+    if ((int)(blockIdx.x + gridDim.x) < items) issue(blockIdx.x + gridDim.x, 1);
+  }
 
   const int tid = threadIdx.x;
   const int ln = tid / TPL, lt = tid - ln * TPL;
   const int comp = ln / RPB, rr = ln - comp * RPB;  // line = (species, interior row)
-  const int row = i0 + rr;
-  const int f = b * 2 + comp;
-  const long long base = (long long)f * sp.npts + (long long)row * N;
-  double2* S = Sbase + ln * F::SL;
-  const double* kin = sp.kin + (long long)b * sp.nparams;
-  const double* Wc = Wst + comp * (RPB + 2) * N;
-  const double* Wu = Wst;
-  const double* Wv = Wst + (RPB + 2) * N;
-
   const CompCoef kc = comp_coef<0>(sp, comp, 0, N);
-  RowCoef rc;
-  {
-    const double* bands = sp.rho_b + (long long)comp * 3 * n1;
-    rc.a = bands[row];
-    rc.b = (row < n1 - 1) ? bands[n1 + row] : 0.0;
-    rc.c = (row > 0) ? bands[2 * n1 + row - 1] : 0.0;
-    rc.d = sp.d_rho[comp * n1 + row];
-  }
-  auto fval = [&](int t) -> double {
-    double u = Wu[(rr + 1) * N + t], v = Wv[(rr + 1) * N + t];
-    if (sp.lift[0] != 0.0) u = __dadd_rn(u, sp.lift[0]);
-    if (sp.lift[1] != 0.0) v = __dadd_rn(v, sp.lift[1]);
-    double g0, g1;
-    reaction<KIN>(kin, u, v, g0, g1);
-    const double d = kc.coeff * diffusion_rows<0>(kc, rc, Wc, rr, t, N);
-    return __dadd_rn(d, comp == 0 ? g0 : g1);
-  };
+  const double lift0 = sp.lift[0], lift1 = sp.lift[1];
+  mbar_wait(&full[2], 0);
 
-  // ---- forward phase A with F evaluated on the fly (columns n2 = lt, lt + TPL, ...)
-  double2 keepa[M2 / TPL][M1];
+  int t = 0;
+  for (int item = blockIdx.x; item < items; item += gridDim.x, ++t) {
+    const int k = t & 1;
+    const int b = item / per;
+    const int i0 = (item - b * per) * RPB;
+    const int row = i0 + rr;
+    const int f = b * 2 + comp;
+    uint8_t* bb = bufs + k * D::buf;
+    const double* Wst = reinterpret_cast<const double*>(bb);
+    const double* phs = reinterpret_cast<const double*>(bb + D::reg_a);
+    double kin[9];
 #pragma unroll
-  for (int q = 0; q < M2 / TPL; ++q) {
-    const int n2 = lt + q * TPL;
-#pragma unroll
-    for (int n1i = 0; n1i < M1; ++n1i) {
-      const int k = n2 + M2 * n1i;
-      keepa[q][n1i] = make_double2(fval(2 * k), fval(2 * k + 1));
+    for (int q = 0; q < 9; ++q) kin[q] = (q < sp.nparams) ? __ldg(sp.kin + (long long)b * sp.nparams + q) : 0.0;
+    RowCoef rc;
+    {
+      const double* bands = sp.rho_b + (long long)comp * 3 * n1;
+      rc.a = __ldg(bands + row);
+      rc.b = (row < n1 - 1) ? __ldg(bands + n1 + row) : 0.0;
+      rc.c = (row > 0) ? __ldg(bands + 2 * n1 + row - 1) : 0.0;
+      rc.d = __ldg(sp.d_rho + comp * n1 + row);
     }
-  }
+    mbar_wait(&full[k], (t >> 1) & 1);
+
+    const double* Wc = Wst + (size_t)comp * (RPB + 2) * N;
+    const double* Wu = Wst;
+    const double* Wv = Wst + (size_t)(RPB + 2) * N;
+    auto fval = [&](int x) -> double {
+      double u = Wu[(rr + 1) * N + x], v = Wv[(rr + 1) * N + x];
+      if (lift0 != 0.0) u = __dadd_rn(u, lift0);
+      if (lift1 != 0.0) v = __dadd_rn(v, lift1);
+      double g0, g1;
+      reaction<KIN>(kin, u, v, g0, g1);
+      const double d = kc.coeff * diffusion_rows<0>(kc, rc, Wc, rr, x, N);
+      return __dadd_rn(d, comp == 0 ? g0 : g1);
+    };
+    // ---- F on the fly, in forward phase A order (columns n2 = lt, lt + TPL, ...)
+    double2 keepa[M2 / TPL][M1];
 #pragma unroll
-  for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, false>(keepa[q], S, lt + q * TPL, tp.tw);
-  theta_tail<M1, M2, false>(tp, S, lt, row, 0, comp, f, base, 1, 1);
+    for (int q = 0; q < M2 / TPL; ++q) {
+      const int n2 = lt + q * TPL;
+#pragma unroll
+      for (int n1i = 0; n1i < M1; ++n1i) {
+        const int kk = n2 + M2 * n1i;
+        keepa[q][n1i] = make_double2(fval(2 * kk), fval(2 * kk + 1));
+      }
+    }
+    __syncthreads();  // every line's F is in registers: the W stage may be overwritten
+    double2* S = reinterpret_cast<double2*>(bb) + ln * F::SL;
+#pragma unroll
+    for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, false, true>(keepa[q], S, lt + q * TPL, tw_s);
+    const long long obase = (long long)f * fsz + (long long)row * N;
+    theta_tail<M1, M2, false, true>(tp, S, lt, phs + (size_t)ln * (M + 1), tw_s, f, obase, 1, 1);
+    // release buffer k: generic-proxy accesses before the async-proxy refill
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0 && item + 2 * (int)gridDim.x < items) issue(item + 2 * gridDim.x, k);
+  }
 }
 
 }  // namespace cg

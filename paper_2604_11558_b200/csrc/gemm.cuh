@@ -82,7 +82,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
   constexpr int EPIB = StageBytes<BM, BN>::epi;
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the shared array (an integer round trip
+  // would hide the address space and turn every fragment load into a generic LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   double* etile = reinterpret_cast<double*>(smem + STAGES * STAGE);  // [BM][BN]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE + EPIB);
   uint64_t* empty = full + STAGES;
@@ -253,6 +255,12 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
       col_in8 = 2 * tq;
     }
     const int row_in8 = (VAR == VAR_TN) ? perm8(g) : g;
+    // Epilogue column rotation: odd row groups take fragment j^1 in step j, so
+    // a quarter-warp's 16-byte accesses to the dense [BM][BN] tile cover all
+    // eight bank groups (plain order: every row group hit the same banks,
+    // 8-way conflicts on the W reads and the staging writes).
+    static_assert(NT % 2 == 0, "epilogue rotation pairs fragments j and j^1");
+    const bool rot = (g & 1) != 0;
 
     if (EPI == EPI_AXPY)
       mbar_wait(epi_full, tc & 1);  // W tile is in etile
@@ -277,7 +285,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
           const double* phirow = p.phi + c * p.phi_c + s * p.phi_s + (long long)(m / p.phi_rdiv) * p.phi_m;
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
-            int n = n0 + wn0 + j * 8 + col_in8;
+            int n = n0 + wn0 + (j ^ (int)rot) * 8 + col_in8;
             if (n >= p.N) n = 0;
             const int n_hi = (n + 1 < p.N) ? n + 1 : n;  // odd N: the pair's second column is padding
             ph[ii][j].x = __ldg(phirow + (long long)n * p.phi_n);
@@ -291,9 +299,10 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
         const int ml = wm0 + i * 8 + row_in8;
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
-          const int nl = wn0 + j * 8 + col_in8;
+          const int nl = wn0 + (j ^ (int)rot) * 8 + col_in8;
           double2* slot = reinterpret_cast<double2*>(etile + ml * BN + nl);
-          double v0 = acc[i][j][0], v1 = acc[i][j][1];
+          double v0 = rot ? acc[i][j ^ 1][0] : acc[i][j][0];
+          double v1 = rot ? acc[i][j ^ 1][1] : acc[i][j][1];
           if (EPI == EPI_PHI) {
             v0 *= ph[ii][j].x;
             v1 *= ph[ii][j].y;

@@ -11,6 +11,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -275,9 +276,7 @@ struct cg_plan {
   std::vector<GraphEntry> graphs;
   cudaStream_t cap_stream = nullptr;
   // disk + FFT theta + built-in kinetics: F-build and stages[0] (theta) run
-  // as one fused kernel (fused_disk.cuh) inside cg_run.  Opt-in
-  // (CURVIGPU_FUSED_FRONT=1): measured slower than the two separate kernels
-  // on B200 so far (profiles/r01_v6_fused_vs_unfused.txt)
+  // as one persistent fused kernel (fused_disk.cuh) inside cg_run
   bool fused_front = false;
   int fused_m1 = 0, fused_m2 = 0;
 };
@@ -586,7 +585,15 @@ int launch_fused_t(const ThetaParams& tp, const StencilParams& sp, cudaStream_t 
                                   (int)D::smem));
     return CG_OK;
   }
-  const unsigned blocks = (unsigned)(sp.batch * (sp.n1 / D::RPB));
+  // persistent: one CTA per SM walks the (run, RPB-row block) items
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const long long items = (long long)sp.batch * (sp.n1 / D::RPB);
+  const unsigned blocks = (unsigned)std::min<long long>(items, num_sms);
   disk_ftheta_kernel<M1, M2, KIN><<<blocks, 256, D::smem, s>>>(tp, sp);
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
@@ -637,7 +644,6 @@ int launch_fused_front(cg_plan* p, const double* Win, bool count_step, cudaStrea
   sp.step = count_step ? p->step_dev : nullptr;
   if (p->fused_m1 == 8 && p->fused_m2 == 16) return launch_fused_k<8, 16>(p->kin, tp, sp, s, conf);
   if (p->fused_m1 == 8 && p->fused_m2 == 8) return launch_fused_k<8, 8>(p->kin, tp, sp, s, conf);
-  if (p->fused_m1 == 16 && p->fused_m2 == 16) return launch_fused_k<16, 16>(p->kin, tp, sp, s, conf);
   return launch_fused_k<4, 8>(p->kin, tp, sp, s, conf);
 }
 
@@ -666,17 +672,19 @@ int launch_step(cg_plan* p, const double* Win, double* Wout, const double* Gext,
   return CG_OK;
 }
 
-// Decide whether the disk front end can run fused (after build_stages).
+// Decide whether the disk front end runs fused (after build_stages): disk,
+// built-in two-species kinetics, FFT theta with N in {64, 128, 256} and rho
+// rows a multiple of the item height.  CURVIGPU_NO_FUSED_FRONT=1 keeps the
+// two separate kernels (measurement / A-B comparison).
 int setup_fused_front(cg_plan* p) {
   if (p->geom != CG_DISK || p->padded || p->kin == CG_KIN_EXTERNAL || p->C != 2 || p->stages.empty() ||
-      p->stages[0].var != VAR_THETA || !getenv("CURVIGPU_FUSED_FRONT"))
+      p->stages[0].var != VAR_THETA || getenv("CURVIGPU_NO_FUSED_FRONT"))
     return CG_OK;
   const int M = p->n2 / 2;
   int m1 = 0, m2 = 0;
   if (M == 32) m1 = 4, m2 = 8;
   if (M == 64) m1 = 8, m2 = 8;
   if (M == 128) m1 = 8, m2 = 16;
-  if (M == 256) m1 = 16, m2 = 16;
   if (!m1) return CG_OK;
   const int lpb = 256 / (m1 < m2 ? m1 : m2);  // FastTheta::LPB
   if (p->n1 % (lpb / 2) != 0) return CG_OK;

@@ -349,13 +349,23 @@ struct FastTheta {
   static constexpr size_t smem = (size_t)LPB * SL * sizeof(double2);
 };
 
+// table read: read-only global path, or shared memory (TS) when a kernel
+// stages the Phi rows and twiddles itself
+template <bool TS, typename T>
+__device__ __forceinline__ T ldt(const T* p) {
+  if constexpr (TS)
+    return *p;
+  else
+    return __ldg(p);
+}
+
 // forward phase A for column n2: M1 loaded values -> DFT_M1 -> twiddle -> S
-template <int M1, int M2, bool INV>
+template <int M1, int M2, bool INV, bool TS = false>
 __device__ __forceinline__ void phase_a(double2* r, double2* S, int n2, const double2* tw) {
   dft_reg<M1, INV>(r);
 #pragma unroll
   for (int k1 = 1; k1 < M1; ++k1) {
-    const double2 w = __ldg(tw + 2 * n2 * k1);  // w_M^(n2 k1) from the length-2M table
+    const double2 w = ldt<TS>(tw + 2 * n2 * k1);  // w_M^(n2 k1) from the length-2M table
     r[k1] = cmul(r[k1], INV ? cconj(w) : w);
   }
 #pragma unroll
@@ -365,14 +375,15 @@ __device__ __forceinline__ void phase_a(double2* r, double2* S, int n2, const do
 // Everything after forward phase A (every column's M1 twiddled values are in
 // S's padded transpose layout, not yet synchronised): forward phase B, real
 // split, Phi, merge, inverse FFT, scaled store (+ W + tau*y and the guard).
-template <int M1, int M2, bool AXPY>
-__device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int lt, int la, int lbc, int c, int f,
-                                           long long base, long long es, int Bc) {
+// ph = this line's Phi_j row (M + 1 values), tw = the N twiddles; both in
+// global memory, or in shared memory when TS.
+template <int M1, int M2, bool AXPY, bool TS = false>
+__device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int lt, const double* ph,
+                                           const double2* tw, int f, long long base, long long es, int Bc) {
   using F = FastTheta<M1, M2>;
   constexpr int M = F::M, TPL = F::TPL;
   constexpr int RMAX = M1 > M2 ? M1 : M2;
   double2 r[RMAX];
-  const double2* tw = p.tw;
   __syncthreads();
   // ---------------- forward phase B: rows k1 = lt, lt + TPL, ...
   double2 keep[M1 / TPL][M2];
@@ -393,13 +404,11 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
   __syncthreads();
   // ---------------- split to X_j, scale by Phi_j, merge to Z'_j (pairs j, M-j)
   {
-    const int cls = p.phi_class_a == 1 ? la : (p.phi_class_a == 0 ? lbc : la * Bc + lbc);
-    const double* ph = p.phif + ((long long)c * p.nclass + cls) * (M + 1);
     for (int j = lt; j <= M / 2; j += TPL) {
       if (j == 0) {
         const double2 z0 = S[0];
-        const double x0 = (z0.x + z0.y) * __ldg(ph);
-        const double xm = (z0.x - z0.y) * __ldg(ph + M);
+        const double x0 = (z0.x + z0.y) * ldt<TS>(ph);
+        const double xm = (z0.x - z0.y) * ldt<TS>(ph + M);
         S[0] = make_double2(0.5 * (x0 + xm), 0.5 * (x0 - xm));
         continue;
       }
@@ -407,9 +416,9 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
       const double2 zj = S[j], zm = S[jm];
       const double2 e = make_double2(0.5 * (zj.x + zm.x), 0.5 * (zj.y - zm.y));
       const double2 o = make_double2(0.5 * (zj.y + zm.y), -0.5 * (zj.x - zm.x));
-      const double2 wj = __ldg(tw + j);
+      const double2 wj = ldt<TS>(tw + j);
       const double2 wo = cmul(wj, o);
-      const double pj = __ldg(ph + j), pm = __ldg(ph + jm);
+      const double pj = ldt<TS>(ph + j), pm = ldt<TS>(ph + jm);
       const double2 xj = make_double2((e.x + wo.x) * pj, (e.y + wo.y) * pj);
       const double2 xmj = make_double2((e.x - wo.x) * pm, -(e.y - wo.y) * pm);
       const double2 s1 = make_double2(0.5 * (xj.x + xmj.x), 0.5 * (xj.y - xmj.y));
@@ -435,7 +444,7 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
   }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, true>(keepa[q], S, lt + q * TPL, tw);
+  for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, true, TS>(keepa[q], S, lt + q * TPL, tw);
   __syncthreads();
   // ---------------- inverse phase B + store (y_2k = Re z'_k / M, y_2k+1 = Im z'_k / M)
   bool bad = false;
@@ -530,7 +539,9 @@ __global__ void __launch_bounds__(256) theta_fast_kernel(const ThetaParams p) {
   }
 #pragma unroll
   for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, false>(keepa[q], S, lt + q * TPL, p.tw);
-  theta_tail<M1, M2, AXPY>(p, S, lt, la, lbc, c, f, base, es, Bc);
+  const int cls = p.phi_class_a == 1 ? la : (p.phi_class_a == 0 ? lbc : la * Bc + lbc);
+  const double* ph = p.phif + ((long long)c * p.nclass + cls) * (M + 1);
+  theta_tail<M1, M2, AXPY>(p, S, lt, ph, p.tw, f, base, es, Bc);
 }
 
 }  // namespace cg
