@@ -14,12 +14,14 @@
 // read W + write F + read F + write T for fbuild_rows + theta_fast.
 #pragma once
 
+#include <type_traits>
+
 #include "stencil.cuh"
 #include "thetafft.cuh"
 
 namespace cg {
 
-template <int M1, int M2>
+template <int M1, int M2, int NBUF = 2>
 struct FusedDisk {
   using F = FastTheta<M1, M2>;
   static constexpr int M = F::M;
@@ -29,30 +31,37 @@ struct FusedDisk {
   static constexpr size_t wst = (size_t)2 * (RPB + 2) * N * sizeof(double);   // staged W rows
   static constexpr size_t sft = (size_t)LPB * F::SL * sizeof(double2);        // FFT tile (overlays W)
   static constexpr size_t reg_a = ((wst > sft ? wst : sft) + 127) / 128 * 128;
-  static constexpr size_t phib = (size_t)LPB * (M + 1) * sizeof(double);     // Phi rows of the item
+  static constexpr int PS = ((M + 1 + 7) / 8 * 8) % 16 == 0 ? (M + 1 + 7) / 8 * 8 + 8 : (M + 1 + 7) / 8 * 8;
+  static constexpr size_t phib = (size_t)LPB * PS * sizeof(double);          // scaled Phi rows of the item
   static constexpr size_t buf = reg_a + (phib + 127) / 128 * 128;
   static constexpr size_t twb = (size_t)N * sizeof(double2);
-  static constexpr size_t smem = 128 + twb + 2 * buf + 64;                    // + alignment slack, barriers
+  static constexpr size_t twab = (size_t)M * sizeof(double2);  // phase-A twiddles as [M1][M2]
+  static constexpr size_t smem = 128 + twb + twab + NBUF * buf + 64;          // + alignment slack, barriers
   static_assert(RPB % 2 == 0, "Phi row blocks must stay 16-byte aligned");
 };
 
-template <int M1, int M2, int KIN>
-__global__ void __launch_bounds__(256, 1) disk_ftheta_kernel(const ThetaParams tp, const StencilParams sp) {
+// NBUF = 2: one CTA per SM, item t+2 prefetched into the buffer item t frees.
+// NBUF = 1: two CTAs per SM (register-capped), each refilling its single
+// buffer after its item; the other CTA's arithmetic covers the refill.
+template <int M1, int M2, int KIN, int NBUF>
+__global__ void __launch_bounds__(256, 3 - NBUF) disk_ftheta_kernel(const ThetaParams tp, const StencilParams sp) {
   using F = FastTheta<M1, M2>;
-  using D = FusedDisk<M1, M2>;
+  using D = FusedDisk<M1, M2, NBUF>;
   constexpr int M = F::M, TPL = F::TPL, RPB = D::RPB, N = D::N;
   extern __shared__ uint8_t fd_raw[];
   uint8_t* base_s = fd_raw + ((128u - (smem_u32(fd_raw) & 127u)) & 127u);  // stays a shared-space pointer
   double2* tw_s = reinterpret_cast<double2*>(base_s);
-  uint8_t* bufs = base_s + D::twb;
-  uint64_t* full = reinterpret_cast<uint64_t*>(bufs + 2 * D::buf);  // [2] item buffers, [2] twiddles
+  double2* twa_s = reinterpret_cast<double2*>(base_s + D::twb);
+  uint8_t* bufs = base_s + D::twb + D::twab;
+  uint64_t* full = reinterpret_cast<uint64_t*>(bufs + NBUF * D::buf);  // [NBUF] item buffers, [2] twiddles
 
   const int n1 = sp.n1;
   const int per = n1 / RPB;
   const int items = sp.batch * per;
   const long long fsz = sp.npts;  // disk plans are never padded here
   const uint32_t row_bytes = N * sizeof(double);
-  const uint32_t item_bytes = (uint32_t)(2 * (RPB + 2) * row_bytes + 2 * RPB * (M + 1) * sizeof(double));
+  constexpr int PS = D::PS;  // == tp.phis_ld (checked at plan set-up)
+  const uint32_t item_bytes = (uint32_t)(2 * (RPB + 2) * row_bytes + 2 * RPB * PS * sizeof(double));
 
   if (sp.step && blockIdx.x == 0 && threadIdx.x == 0) *sp.step += 1;
 
@@ -75,8 +84,8 @@ __global__ void __launch_bounds__(256, 1) disk_ftheta_kernel(const ThetaParams t
                    &full[k]);
       if (i0 == 0) bulk_load_1d(dst, src, row_bytes, &full[k]);
       if (i0 + RPB >= n1) bulk_load_1d(dst + (size_t)(RPB + 1) * N, src + (long long)(n1 - 1) * N, row_bytes, &full[k]);
-      bulk_load_1d(phs + (size_t)comp * RPB * (M + 1), tp.phif + ((long long)comp * tp.nclass + i0) * (M + 1),
-                   (uint32_t)(RPB * (M + 1) * sizeof(double)), &full[k]);
+      bulk_load_1d(phs + (size_t)comp * RPB * PS, tp.phis + ((long long)comp * tp.nclass + i0) * PS,
+                   (uint32_t)(RPB * PS * sizeof(double)), &full[k]);
     }
   };
 
@@ -91,7 +100,7 @@ __global__ void __launch_bounds__(256, 1) disk_ftheta_kernel(const ThetaParams t
     mbar_arrive_expect_tx(&full[2], (uint32_t)D::twb);
     bulk_load_1d(tw_s, tp.tw, (uint32_t)D::twb, &full[2]);
     if ((int)blockIdx.x < items) issue(blockIdx.x, 0);
-    if ((int)(blockIdx.x + gridDim.x) < items) issue(blockIdx.x + gridDim.x, 1);
+    if (NBUF == 2 && (int)(blockIdx.x + gridDim.x) < items) issue(blockIdx.x + gridDim.x, 1);
   }
 
   const int tid = threadIdx.x;
@@ -100,10 +109,12 @@ __global__ void __launch_bounds__(256, 1) disk_ftheta_kernel(const ThetaParams t
   const CompCoef kc = comp_coef<0>(sp, comp, 0, N);
   const double lift0 = sp.lift[0], lift1 = sp.lift[1];
   mbar_wait(&full[2], 0);
+  for (int i = threadIdx.x; i < M; i += blockDim.x) twa_s[i] = tw_s[2 * (i % M2) * (i / M2)];
+  __syncthreads();
 
   int t = 0;
   for (int item = blockIdx.x; item < items; item += gridDim.x, ++t) {
-    const int k = t & 1;
+    const int k = NBUF == 2 ? (t & 1) : 0;
     const int b = item / per;
     const int i0 = (item - b * per) * RPB;
     const int row = i0 + rr;
@@ -122,41 +133,69 @@ __global__ void __launch_bounds__(256, 1) disk_ftheta_kernel(const ThetaParams t
       rc.c = (row > 0) ? __ldg(bands + 2 * n1 + row - 1) : 0.0;
       rc.d = __ldg(sp.d_rho + comp * n1 + row);
     }
-    mbar_wait(&full[k], (t >> 1) & 1);
+    mbar_wait(&full[k], NBUF == 2 ? ((t >> 1) & 1) : (t & 1));
 
-    const double* Wc = Wst + (size_t)comp * (RPB + 2) * N;
-    const double* Wu = Wst;
-    const double* Wv = Wst + (size_t)(RPB + 2) * N;
-    auto fval = [&](int x) -> double {
-      double u = Wu[(rr + 1) * N + x], v = Wv[(rr + 1) * N + x];
-      if (lift0 != 0.0) u = __dadd_rn(u, lift0);
-      if (lift1 != 0.0) v = __dadd_rn(v, lift1);
-      double g0, g1;
-      reaction<KIN>(kin, u, v, g0, g1);
-      const double d = kc.coeff * diffusion_rows<0>(kc, rc, Wc, rr, x, N);
-      return __dadd_rn(d, comp == 0 ? g0 : g1);
+    const double* Wc = Wst + (size_t)comp * (RPB + 2) * N;             // this species' staged rows
+    const double* Wo = Wst + (size_t)(1 - comp) * (RPB + 2) * N;       // the other species'
+    const double* rowc = Wc + (rr + 1) * N;
+    // F at the point pair (2kk, 2kk+1): one 16-byte load each for the row,
+    // the rows above and below and the other species, plus the two outer
+    // theta neighbours; same arithmetic as diffusion_rows<0> + the F-build
+    // reaction, so the values equal fbuild_rows_kernel's bit for bit.
+    auto fpair = [&](auto compc, int kk) -> double2 {
+      constexpr int CMP = decltype(compc)::value;  // species, compile-time: the other reaction term is dead code
+      const int x = 2 * kk;
+      const double2 c2 = *reinterpret_cast<const double2*>(rowc + x);
+      const double2 m2 = *reinterpret_cast<const double2*>(rowc - N + x);
+      const double2 p2 = *reinterpret_cast<const double2*>(rowc + N + x);
+      const double2 o2 = *reinterpret_cast<const double2*>(Wo + (rr + 1) * N + x);
+      const double xl = rowc[x == 0 ? N - 1 : x - 1];
+      const double xr = rowc[x + 2 == N ? 0 : x + 2];
+      double2 out;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double x0 = h ? c2.y : c2.x, xm = h ? m2.y : m2.x, xp = h ? p2.y : p2.x;
+        const double left = h ? c2.x : xl, right = h ? xr : c2.y;
+        const double rrv = rc.a * x0 + rc.c * xm + rc.b * xp;
+        const double q = kc.th_off * left + kc.th_diag * x0 + kc.th_off * right;
+        const double d = kc.coeff * (rrv + rc.d * q);
+        double u = CMP == 0 ? x0 : (h ? o2.y : o2.x);
+        double v = CMP == 0 ? (h ? o2.y : o2.x) : x0;
+        if (lift0 != 0.0) u = __dadd_rn(u, lift0);
+        if (lift1 != 0.0) v = __dadd_rn(v, lift1);
+        double g0, g1;
+        reaction<KIN>(kin, u, v, g0, g1);
+        const double val = __dadd_rn(d, CMP == 0 ? g0 : g1);
+        if (h)
+          out.y = val;
+        else
+          out.x = val;
+      }
+      return out;
     };
     // ---- F on the fly, in forward phase A order (columns n2 = lt, lt + TPL, ...)
     double2 keepa[M2 / TPL][M1];
 #pragma unroll
     for (int q = 0; q < M2 / TPL; ++q) {
       const int n2 = lt + q * TPL;
+      if (comp == 0) {  // warp-uniform (a warp's lines share the species)
 #pragma unroll
-      for (int n1i = 0; n1i < M1; ++n1i) {
-        const int kk = n2 + M2 * n1i;
-        keepa[q][n1i] = make_double2(fval(2 * kk), fval(2 * kk + 1));
+        for (int n1i = 0; n1i < M1; ++n1i) keepa[q][n1i] = fpair(std::integral_constant<int, 0>{}, n2 + M2 * n1i);
+      } else {
+#pragma unroll
+        for (int n1i = 0; n1i < M1; ++n1i) keepa[q][n1i] = fpair(std::integral_constant<int, 1>{}, n2 + M2 * n1i);
       }
     }
     __syncthreads();  // every line's F is in registers: the W stage may be overwritten
     double2* S = reinterpret_cast<double2*>(bb) + ln * F::SL;
 #pragma unroll
-    for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, false, true>(keepa[q], S, lt + q * TPL, tw_s);
+    for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, false, true, true>(keepa[q], S, lt + q * TPL, twa_s);
     const long long obase = (long long)f * fsz + (long long)row * N;
-    theta_tail<M1, M2, false, true>(tp, S, lt, phs + (size_t)ln * (M + 1), tw_s, f, obase, 1, 1);
+    theta_tail<M1, M2, false, true>(tp, S, lt, phs + (size_t)ln * PS, tw_s, f, obase, 1, 1, twa_s);
     // release buffer k: generic-proxy accesses before the async-proxy refill
     fence_proxy_async_smem();
     __syncthreads();
-    if (threadIdx.x == 0 && item + 2 * (int)gridDim.x < items) issue(item + 2 * gridDim.x, k);
+    if (threadIdx.x == 0 && item + NBUF * (int)gridDim.x < items) issue(item + NBUF * gridDim.x, k);
   }
 }
 

@@ -240,6 +240,8 @@ struct Stage {
   // VAR_THETA: field = [A][N][Bc], W lines per CTA, Phi_j table, twiddles
   int tA, tBc, tW, tclass_mode, tnclass;
   const double* phif;
+  const double* phis;  // pre-scaled, padded rows (ThetaParams::phis)
+  int phis_ld;
   const double2* tw;
 };
 
@@ -381,6 +383,14 @@ double* buf_ptr(cg_plan* p, int id, double* out) { return id == BUF_X ? p->X : i
 
 bool pow2(int n) { return n >= 4 && (n & (n - 1)) == 0; }
 
+// row stride of the scaled Phi table: M + 1 rounded up to a multiple of 8
+// doubles that is an odd multiple of 8 (two lines 64 bytes apart per half-warp)
+int phis_stride(int M) {
+  int ps = (M + 1 + 7) / 8 * 8;
+  if (ps % 16 == 0) ps += 8;
+  return ps;
+}
+
 // FFT theta-propagator stage over fields viewed as [A][N][Bc].  phi_at(c, cls,
 // col) returns Phi for component c, line class cls and eigen-column col; the
 // kernel takes Phi_j = Phi[col(j)] per frequency j = 0..N/2.
@@ -412,6 +422,17 @@ int add_theta_stage(cg_plan* p, int epi, int src, int dst, int N, int A, int Bc,
   double* phif = nullptr;
   int rc = upload(p, h.data(), h.size(), &phif);
   if (rc) return rc;
+  // scaled copy for the register FFT kernels: exact power-of-two factors
+  // (1/(2M) at j = 0, M; 1/(4M) otherwise), rows padded to an odd multiple of 8
+  const int ps = phis_stride(M);
+  std::vector<double> hs((size_t)p->C * nclass * ps, 0.0);
+  for (size_t r = 0; r < (size_t)p->C * nclass; ++r)
+    for (int j = 0; j <= M; ++j)
+      hs[r * ps + j] = h[r * (M + 1) + j] * ((j == 0 || j == M) ? 0.5 : 0.25) / (double)M;
+  double* phis = nullptr;
+  if ((rc = upload(p, hs.data(), hs.size(), &phis))) return rc;
+  st.phis = phis;
+  st.phis_ld = ps;
   std::vector<double> tw(2 * (size_t)N);
   for (int t = 0; t < N; ++t) {
     const double ang = 2.0 * M_PI * (double)t / (double)N;
@@ -469,6 +490,8 @@ int launch_theta(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
   tp.phi_class_a = st.tclass_mode;
   tp.nclass = st.tnclass;
   tp.phif = st.phif;
+  tp.phis = st.phis;
+  tp.phis_ld = st.phis_ld;
   tp.tw = st.tw;
   tp.X = buf_ptr(p, st.src, Wout);
   tp.Y = buf_ptr(p, st.dst, Wout);
@@ -577,15 +600,15 @@ int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
 }
 
 // Launch one full step: Win (+G) -> F -> stage chain -> Wout.
-template <int M1, int M2, int KIN>
-int launch_fused_t(const ThetaParams& tp, const StencilParams& sp, cudaStream_t s, bool configure_only) {
-  using D = FusedDisk<M1, M2>;
+template <int M1, int M2, int KIN, int NBUF>
+int launch_fused_nb(const ThetaParams& tp, const StencilParams& sp, cudaStream_t s, bool configure_only) {
+  using D = FusedDisk<M1, M2, NBUF>;
   if (configure_only) {
-    CUDA_TRY(cudaFuncSetAttribute(disk_ftheta_kernel<M1, M2, KIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(disk_ftheta_kernel<M1, M2, KIN, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)D::smem));
     return CG_OK;
   }
-  // persistent: one CTA per SM walks the (run, RPB-row block) items
+  // persistent: (3 - NBUF) CTAs per SM walk the (run, RPB-row block) items
   static int num_sms = 0;
   if (!num_sms) {
     int dev = 0;
@@ -593,10 +616,17 @@ int launch_fused_t(const ThetaParams& tp, const StencilParams& sp, cudaStream_t 
     CUDA_TRY(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const long long items = (long long)sp.batch * (sp.n1 / D::RPB);
-  const unsigned blocks = (unsigned)std::min<long long>(items, num_sms);
-  disk_ftheta_kernel<M1, M2, KIN><<<blocks, 256, D::smem, s>>>(tp, sp);
+  const unsigned blocks = (unsigned)std::min<long long>(items, (long long)num_sms * (3 - NBUF));
+  disk_ftheta_kernel<M1, M2, KIN, NBUF><<<blocks, 256, D::smem, s>>>(tp, sp);
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
+}
+
+template <int M1, int M2, int KIN>
+int launch_fused_t(const ThetaParams& tp, const StencilParams& sp, cudaStream_t s, bool configure_only) {
+  static const int nbuf = getenv("CURVIGPU_FUSED_NBUF") ? atoi(getenv("CURVIGPU_FUSED_NBUF")) : 1;
+  if (nbuf == 1) return launch_fused_nb<M1, M2, KIN, 1>(tp, sp, s, configure_only);
+  return launch_fused_nb<M1, M2, KIN, 2>(tp, sp, s, configure_only);
 }
 
 template <int M1, int M2>
@@ -623,6 +653,8 @@ int launch_fused_front(cg_plan* p, const double* Win, bool count_step, cudaStrea
   tp.phi_class_a = st.tclass_mode;
   tp.nclass = st.tnclass;
   tp.phif = st.phif;
+  tp.phis = st.phis;
+  tp.phis_ld = st.phis_ld;
   tp.tw = st.tw;
   tp.Y = buf_ptr(p, st.dst, nullptr);
   StencilParams sp{};

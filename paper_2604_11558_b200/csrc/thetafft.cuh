@@ -36,6 +36,11 @@ struct ThetaParams {
   int phi_class_a;   // Phi class of a line: 1 = a (disk, cylinder), 0 = bc (sphere), 2 = a*Bc + bc (ball)
   int nclass;        // classes per component
   const double* phif;  // [C][nclass][N/2 + 1] Phi_j
+  // the same values pre-scaled for theta_tail (Phi_0, Phi_M by 1/(2M), the
+  // rest by 1/(4M): exact powers of two that absorb the split/merge halves
+  // and the inverse 1/M), rows padded to phis_ld (bank-conflict free in smem)
+  const double* phis;
+  int phis_ld;
   const double2* tw;   // [N] exp(-2 pi i t / N)
   const double* X;
   double* Y;
@@ -359,13 +364,16 @@ __device__ __forceinline__ T ldt(const T* p) {
     return __ldg(p);
 }
 
-// forward phase A for column n2: M1 loaded values -> DFT_M1 -> twiddle -> S
-template <int M1, int M2, bool INV, bool TS = false>
+// forward phase A for column n2: M1 loaded values -> DFT_M1 -> twiddle -> S.
+// tw: the length-2M table (w_M^(n2 k1) = tw[2 n2 k1]), or with TA a [M1][M2]
+// table of exactly those values (shared memory: a quarter-warp's lanes then
+// read consecutive entries instead of a stride of 2 k1, bank-conflict free)
+template <int M1, int M2, bool INV, bool TS = false, bool TA = false>
 __device__ __forceinline__ void phase_a(double2* r, double2* S, int n2, const double2* tw) {
   dft_reg<M1, INV>(r);
 #pragma unroll
   for (int k1 = 1; k1 < M1; ++k1) {
-    const double2 w = ldt<TS>(tw + 2 * n2 * k1);  // w_M^(n2 k1) from the length-2M table
+    const double2 w = ldt<TS>(TA ? tw + k1 * M2 + n2 : tw + 2 * n2 * k1);
     r[k1] = cmul(r[k1], INV ? cconj(w) : w);
   }
 #pragma unroll
@@ -379,7 +387,8 @@ __device__ __forceinline__ void phase_a(double2* r, double2* S, int n2, const do
 // global memory, or in shared memory when TS.
 template <int M1, int M2, bool AXPY, bool TS = false>
 __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int lt, const double* ph,
-                                           const double2* tw, int f, long long base, long long es, int Bc) {
+                                           const double2* tw, int f, long long base, long long es, int Bc,
+                                           const double2* twa = nullptr) {
   using F = FastTheta<M1, M2>;
   constexpr int M = F::M, TPL = F::TPL;
   constexpr int RMAX = M1 > M2 ? M1 : M2;
@@ -403,34 +412,33 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
   }
   __syncthreads();
   // ---------------- split to X_j, scale by Phi_j, merge to Z'_j (pairs j, M-j)
+  // ph is the pre-scaled row (ThetaParams::phis): every 1/2 of the textbook
+  // split/merge and the inverse 1/M are folded into it (exact powers of two),
+  // and Z'_{M-j} = conj(s - i w^-j d) reuses the pair's s, d (both exact
+  // identities), so the values equal the unscaled form's
   {
     for (int j = lt; j <= M / 2; j += TPL) {
       if (j == 0) {
         const double2 z0 = S[0];
         const double x0 = (z0.x + z0.y) * ldt<TS>(ph);
         const double xm = (z0.x - z0.y) * ldt<TS>(ph + M);
-        S[0] = make_double2(0.5 * (x0 + xm), 0.5 * (x0 - xm));
+        S[0] = make_double2(x0 + xm, x0 - xm);
         continue;
       }
       const int jm = M - j;
       const double2 zj = S[j], zm = S[jm];
-      const double2 e = make_double2(0.5 * (zj.x + zm.x), 0.5 * (zj.y - zm.y));
-      const double2 o = make_double2(0.5 * (zj.y + zm.y), -0.5 * (zj.x - zm.x));
+      const double2 e = make_double2(zj.x + zm.x, zj.y - zm.y);    // 2 E_j
+      const double2 o = make_double2(zj.y + zm.y, zm.x - zj.x);    // 2 O_j
       const double2 wj = ldt<TS>(tw + j);
       const double2 wo = cmul(wj, o);
       const double pj = ldt<TS>(ph + j), pm = ldt<TS>(ph + jm);
       const double2 xj = make_double2((e.x + wo.x) * pj, (e.y + wo.y) * pj);
-      const double2 xmj = make_double2((e.x - wo.x) * pm, -(e.y - wo.y) * pm);
-      const double2 s1 = make_double2(0.5 * (xj.x + xmj.x), 0.5 * (xj.y - xmj.y));
-      const double2 d1 = make_double2(0.5 * (xj.x - xmj.x), 0.5 * (xj.y + xmj.y));
+      const double2 xmj = make_double2((e.x - wo.x) * pm, (wo.y - e.y) * pm);
+      const double2 s1 = make_double2(xj.x + xmj.x, xj.y - xmj.y);
+      const double2 d1 = make_double2(xj.x - xmj.x, xj.y + xmj.y);
       const double2 wd = cmul(cconj(wj), d1);
       S[j] = make_double2(s1.x - wd.y, s1.y + wd.x);
-      if (jm != j) {
-        const double2 s2 = make_double2(0.5 * (xmj.x + xj.x), 0.5 * (xmj.y - xj.y));
-        const double2 d2 = make_double2(0.5 * (xmj.x - xj.x), 0.5 * (xmj.y + xj.y));
-        const double2 wd2 = cmul(make_double2(-wj.x, -wj.y), d2);  // conj(-conj(w^j)) = -w^j
-        S[jm] = make_double2(s2.x - wd2.y, s2.y + wd2.x);
-      }
+      if (jm != j) S[jm] = make_double2(s1.x + wd.y, wd.x - s1.y);
     }
   }
   __syncthreads();
@@ -444,11 +452,15 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
   }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, true, TS>(keepa[q], S, lt + q * TPL, tw);
+  for (int q = 0; q < M2 / TPL; ++q) {
+    if (TS)
+      phase_a<M1, M2, true, true, true>(keepa[q], S, lt + q * TPL, twa);
+    else
+      phase_a<M1, M2, true>(keepa[q], S, lt + q * TPL, tw);
+  }
   __syncthreads();
   // ---------------- inverse phase B + store (y_2k = Re z'_k / M, y_2k+1 = Im z'_k / M)
   bool bad = false;
-  const double scale = 1.0 / (double)M;
 #pragma unroll
   for (int q = 0; q < M1 / TPL; ++q) {
     const int k1 = lt + q * TPL;
@@ -458,7 +470,7 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
 #pragma unroll
     for (int k2 = 0; k2 < M2; ++k2) {
       const int k = k1 + M1 * k2;
-      double y0 = r[k2].x * scale, y1 = r[k2].y * scale;
+      double y0 = r[k2].x, y1 = r[k2].y;  // 1/M is folded into phis
       if (Bc == 1) {
         const long long o = base + 2LL * k;
         if (AXPY) {
@@ -540,7 +552,7 @@ __global__ void __launch_bounds__(256) theta_fast_kernel(const ThetaParams p) {
 #pragma unroll
   for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, false>(keepa[q], S, lt + q * TPL, p.tw);
   const int cls = p.phi_class_a == 1 ? la : (p.phi_class_a == 0 ? lbc : la * Bc + lbc);
-  const double* ph = p.phif + ((long long)c * p.nclass + cls) * (M + 1);
+  const double* ph = p.phis + ((long long)c * p.nclass + cls) * p.phis_ld;
   theta_tail<M1, M2, AXPY>(p, S, lt, ph, p.tw, f, base, es, Bc);
 }
 
