@@ -118,10 +118,15 @@ int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
     const char* ps = getenv("CURVIGPU_SMEM_PAD");
     pad = ps ? atoi(ps) : 0;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem + pad));
+    // full shared-memory carveout: an SM's L1/smem split only changes while it
+    // is idle, so a smaller preferred carveout would keep a kernel running
+    // concurrently on another stream from co-residing
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     int per_sm = 0, dev = 0, sms = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem + pad));
     CUDA_TRY(cudaGetDevice(&dev));
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (const char* cap = getenv("CURVIGPU_GEMM_CPS")) per_sm = std::min(per_sm, std::max(1, atoi(cap)));
     resident = (per_sm > 0 ? per_sm : 1) * sms;
     return CG_OK;
   }
@@ -606,6 +611,8 @@ int launch_fused_nb(const ThetaParams& tp, const StencilParams& sp, cudaStream_t
   if (configure_only) {
     CUDA_TRY(cudaFuncSetAttribute(disk_ftheta_kernel<M1, M2, KIN, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)D::smem));
+    CUDA_TRY(cudaFuncSetAttribute(disk_ftheta_kernel<M1, M2, KIN, NBUF>,
+                                  cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     return CG_OK;
   }
   // persistent: (3 - NBUF) CTAs per SM walk the (run, RPB-row block) items
@@ -616,7 +623,8 @@ int launch_fused_nb(const ThetaParams& tp, const StencilParams& sp, cudaStream_t
     CUDA_TRY(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const long long items = (long long)sp.batch * (sp.n1 / D::RPB);
-  const unsigned blocks = (unsigned)std::min<long long>(items, (long long)num_sms * (3 - NBUF));
+  static const int cps = getenv("CURVIGPU_FRONT_CPS") ? std::max(1, atoi(getenv("CURVIGPU_FRONT_CPS"))) : 3 - NBUF;
+  const unsigned blocks = (unsigned)std::min<long long>(items, (long long)num_sms * std::min(cps, 3 - NBUF));
   disk_ftheta_kernel<M1, M2, KIN, NBUF><<<blocks, 256, D::smem, s>>>(tp, sp);
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
