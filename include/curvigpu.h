@@ -177,6 +177,19 @@ int cg_step_guarded(cg_plan* plan, const double* W, const double* G, double* W_o
 /* Set the plan's device step counter (the next guarded step is step + 1). */
 int cg_plan_set_step(cg_plan* plan, long long step, void* stream);
 
+/* ---- on-device sampling ----
+ * Replaces the per-sample host evaluation of mean_diagnostics()
+ * (models.py:728-744: float(sum(W * weights)) + lift for every component,
+ * weights from quadrature_weights() models.py:675-715, host setup):
+ *   out[f] = sum_i X[f * npts + i] * w[(f % ncls) * npts + i] + (off ? off[f % ncls] : 0)
+ * for nfield consecutive fields of npts values (a [B][C] state with ncls = C).
+ * X, w, off, out, scratch are device pointers; X and w 16-byte aligned;
+ * scratch holds cg_weighted_sums_scratch(nfield, npts) doubles.  Fixed
+ * summation order: reruns are bitwise identical.  Graph-capturable. */
+long long cg_weighted_sums_scratch(long long nfield, long long npts);
+int cg_weighted_sums(const double* X, long long nfield, long long npts, const double* w, int ncls,
+                     const double* off, double* out, double* scratch, long long scratch_len, void* stream);
+
 /* ---- bulk-surface coupled models ----
  * Reaction terms of the reference's two mixed-geometry models from the common
  * state: bulk (u, v) on a ball or cylinder, surface (r, s) on the sphere or

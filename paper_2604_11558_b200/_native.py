@@ -85,6 +85,8 @@ EXPORTS = (
     "cg_coupling_destroy",
     "cg_coupled_kinetics",
     "cg_coupled_run",
+    "cg_weighted_sums_scratch",
+    "cg_weighted_sums",
 )
 
 CG_BS_BALL = 1
@@ -167,6 +169,11 @@ def lib():
     L.cg_coupled_kinetics.restype = ctypes.c_int
     L.cg_coupled_run.argtypes = [vp, vp, vp, vp, vp, ctypes.c_longlong, ctypes.c_longlong, vp, vp]
     L.cg_coupled_run.restype = ctypes.c_int
+    L.cg_weighted_sums_scratch.argtypes = [ctypes.c_longlong, ctypes.c_longlong]
+    L.cg_weighted_sums_scratch.restype = ctypes.c_longlong
+    L.cg_weighted_sums.argtypes = [vp, ctypes.c_longlong, ctypes.c_longlong, vp, ctypes.c_int, vp, vp, vp,
+                                   ctypes.c_longlong, vp]
+    L.cg_weighted_sums.restype = ctypes.c_int
     _lib = L
     return L
 

@@ -26,6 +26,7 @@
 #include "thetafft.cuh"
 #include "fused_disk.cuh"
 #include "coupling.cuh"
+#include "diagnostics.cuh"
 
 using namespace cg;
 
@@ -1202,6 +1203,29 @@ int cg_plan_set_step(cg_plan* p, long long step, void* stream) {
   if (!p) return fail(CG_EINVAL, "null plan");
   if (step < 0 || step > INT_MAX) return fail(CG_EINVAL, "step out of range");
   set_step_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(p->step_dev, (int)step);
+  CUDA_TRY(cudaGetLastError());
+  return CG_OK;
+}
+
+long long cg_weighted_sums_scratch(long long nfield, long long npts) {
+  if (nfield <= 0 || npts <= 0) return 0;
+  return nfield * wsum_segments(npts);
+}
+
+int cg_weighted_sums(const double* X, long long nfield, long long npts, const double* w, int ncls,
+                     const double* off, double* out, double* scratch, long long scratch_len, void* stream) {
+  if (!X || !w || !out || !scratch) return fail(CG_EINVAL, "null argument");
+  if (nfield <= 0 || npts <= 0 || ncls <= 0) return fail(CG_EINVAL, "nfield, npts and ncls must be positive");
+  if (nfield > 65535 || npts > (long long)INT_MAX * 2) return fail(CG_EUNSUPPORTED, "too many fields or points");
+  const long long nseg = wsum_segments(npts);
+  if (scratch_len < nfield * nseg) return fail(CG_EINVAL, "scratch too small (see cg_weighted_sums_scratch)");
+  if ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(w)) & 15)
+    return fail(CG_EINVAL, "X and w must be 16-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  wsum_partial_kernel<<<dim3((unsigned)nseg, (unsigned)nfield), kWsThreads, 0, s>>>(X, npts, w, ncls, scratch,
+                                                                                   (int)nseg);
+  CUDA_TRY(cudaGetLastError());
+  wsum_final_kernel<<<(unsigned)((nfield + 127) / 128), 128, 0, s>>>(scratch, (int)nseg, (int)nfield, ncls, off, out);
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
 }

@@ -140,13 +140,22 @@ class EnsembleResult:
     stop: int
     steps: int
     tau: float
+    times: list | None = None  # sample times (record_every / diagnostics), else None
+    series: object = None  # [R, C, nsamples] integral means on rank 0 (numpy or torch), None elsewhere
 
 
 def run_ensemble(systems, m: int, t_star: float, *, group=None, gather: bool = True,
-                 as_torch: bool = False, raise_on_divergence: bool = False) -> EnsembleResult:
+                 as_torch: bool = False, raise_on_divergence: bool = False,
+                 record_every: int | None = None, diagnostics=None) -> EnsembleResult:
     """Advance every member of ``systems`` (a list of CoupledSystem sharing
     operators) by m steps of tau = t*/m; shard over the torch.distributed
-    group when one is initialised."""
+    group when one is initialised.
+
+    ``diagnostics`` (a ``models.MeanDiagnostics``, e.g.
+    ``mean_diagnostics(systems[0])``) samples every member's integral means on
+    the device at step 0, every ``record_every`` steps and at m, as
+    run_simulation does for one run; the [R, C, nsamples] series is gathered
+    with the fields."""
     import torch
     import torch.distributed as dist
 
@@ -163,6 +172,18 @@ def run_ensemble(systems, m: int, t_star: float, *, group=None, gather: bool = T
     lo, hi = shard_range(R, rank, world)
     mine = systems[lo:hi]
     tau = t_star / m
+    sample_steps = None
+    if diagnostics is not None:
+        from .models import MeanDiagnostics
+
+        if not isinstance(diagnostics, MeanDiagnostics):
+            raise NotImplementedError("ensemble diagnostics must be models.mean_diagnostics(...) (device-evaluated)")
+        every = record_every or m
+        sample_steps = [0]
+        while sample_steps[-1] < m:
+            sample_steps.append(min(m, (sample_steps[-1] // every + 1) * every))
+    names = [c.name for c in systems[0].components]
+    ncomp = len(names)
     if mine:
         _check_shared(mine)
         kin = engine_kinetics(mine[0])
@@ -171,7 +192,16 @@ def run_ensemble(systems, m: int, t_star: float, *, group=None, gather: bool = T
         host = np.stack([np.stack([np.asarray(c.initial, dtype=np.float64) for c in s.components]) for s in mine])
         state = torch.from_numpy(np.ascontiguousarray(host)).to("cuda")
         first_bad = torch.full((hi - lo, plan.ncomp), INT32_MAX, dtype=torch.int32, device="cuda")
-        plan.run(state, 0, m, first_bad)
+        if sample_steps is None:
+            plan.run(state, 0, m, first_bad)
+        else:
+            means = diagnostics.device_means(names, hi - lo)
+            series = torch.empty((len(sample_steps), hi - lo, ncomp), dtype=torch.float64, device="cuda")
+            means.into(state, series[0])
+            for i in range(1, len(sample_steps)):
+                plan.run(state, sample_steps[i - 1], sample_steps[i] - sample_steps[i - 1], first_bad)
+                means.into(state, series[i])
+            series = series.permute(1, 2, 0).contiguous()
         lifts = torch.tensor([float(getattr(c, "lift", 0.0)) for c in mine[0].components],
                              dtype=torch.float64, device="cuda")
         phys = state + lifts.view((1, -1) + (1,) * (state.dim() - 2))
@@ -180,6 +210,8 @@ def run_ensemble(systems, m: int, t_star: float, *, group=None, gather: bool = T
         shape = tuple(systems[0].components[0].ops.shape)
         phys = torch.zeros((0, len(systems[0].components)) + shape, dtype=torch.float64, device="cuda")
         bad = np.zeros((0, len(systems[0].components)), dtype=np.int32)
+        if sample_steps is not None:
+            series = torch.zeros((0, ncomp, len(sample_steps)), dtype=torch.float64, device="cuda")
     if raise_on_divergence and bad.size and bad.min() < INT32_MAX:
         s = int(bad.min())
         raise DivergenceError(f"ensemble run diverged at step {s}", step=s)
@@ -189,4 +221,13 @@ def run_ensemble(systems, m: int, t_star: float, *, group=None, gather: bool = T
         full = phys if rank == 0 else None
     if full is not None and not as_torch:
         full = full.cpu().numpy()
-    return EnsembleResult(full, bad, lo, hi, m, tau)
+    times = full_series = None
+    if sample_steps is not None:
+        times = [k * tau for k in sample_steps]
+        if dist_on and gather and world > 1:
+            full_series = gather_fields(series, R, group=group)
+        else:
+            full_series = series if rank == 0 else None
+        if full_series is not None and not as_torch:
+            full_series = full_series.cpu().numpy()
+    return EnsembleResult(full, bad, lo, hi, m, tau, times, full_series)

@@ -516,6 +516,54 @@ def engine_kinetics(system):
         "paper_2604_11558_b200.models.Kinetics descriptor (no CPU fallback)")
 
 
+def _raise_if_diverged(bad, names):
+    """DivergenceError for the first bad step, naming the first component (in
+    component order) that diverged at it (integrators.py:422-427)."""
+    if bad.min() < INT32_MAX:
+        s = int(bad.min())
+        c = int(np.flatnonzero(bad == s)[0])
+        raise DivergenceError(f"component {names[c]!r} diverged at step {s}", step=s)
+
+
+class _HostSampler:
+    """Host copies of a [1][C][...] device state at sample steps for
+    ``sample_hook`` and arbitrary diagnostics callables, overlapped with the
+    next stepping chunk: ``stage`` snapshots the state on the device (and the
+    divergence flags) and starts the download on a side stream; ``finish``
+    waits for it, raises if the run had diverged by then, and returns the
+    reference's dict of fresh arrays."""
+
+    def __init__(self, state, first_bad, names):
+        import torch
+
+        self.state, self.first_bad, self.names = state, first_bad, names
+        self.snap = torch.empty_like(state)
+        self.host = torch.empty(state.shape, dtype=state.dtype, pin_memory=True)
+        self.bad_dev = torch.empty_like(first_bad)
+        self.bad = torch.empty(first_bad.shape, dtype=first_bad.dtype, pin_memory=True)
+        self.side = torch.cuda.Stream()
+        self.ready = torch.cuda.Event()
+        self.done = torch.cuda.Event()
+
+    def stage(self):
+        import torch
+
+        self.snap.copy_(self.state)
+        self.bad_dev.copy_(self.first_bad)
+        self.ready.record()
+        with torch.cuda.stream(self.side):
+            self.side.wait_event(self.ready)
+            self.host.copy_(self.snap, non_blocking=True)
+            self.bad.copy_(self.bad_dev, non_blocking=True)
+            self.done.record(self.side)
+
+    def finish(self) -> dict:
+        self.done.synchronize()
+        _raise_if_diverged(self.bad.numpy()[0], self.names)
+        host = self.host.numpy()[0]
+        return {n: host[i].copy() for i, n in enumerate(self.names)}
+
+
 def run_simulation(system, m: int, t_star: float, *, record_every: int | None = None,
                    diagnostics: Callable | None = None, sample_hook: Callable | None = None,
                    method: str = "split", as_torch: bool = False) -> RunResult:
@@ -523,9 +571,13 @@ def run_simulation(system, m: int, t_star: float, *, record_every: int | None = 
 
     Kinetics are evaluated from the common state before any component is
     updated; samples are taken at step 0, every ``record_every`` steps and at
-    the final step (host copies only there); the divergence guard runs on the
-    device after every step and raises ``DivergenceError(step)`` naming the
-    first bad step and component, as the reference does.
+    the final step; the divergence guard runs on the device after every step
+    and raises ``DivergenceError(step)`` naming the first bad step and
+    component, as the reference does.  ``diagnostics`` built by
+    ``models.mean_diagnostics`` are evaluated on the device (only the scalars
+    come back, once, at the end); a ``sample_hook`` or any other diagnostics
+    callable gets host copies of the state, downloaded while the next chunk
+    of steps runs.
     """
     import torch
 
@@ -556,40 +608,54 @@ def run_simulation(system, m: int, t_star: float, *, record_every: int | None = 
     state = state.reshape(plan.state_shape).contiguous()
     first_bad = torch.full((1, len(comps)), INT32_MAX, dtype=torch.int32, device="cuda")
     every = record_every or m
-    times: list[float] = []
+    # sample at step 0, every `every` steps and at m (integrators.py:413-430)
+    sample_steps = [0]
+    while sample_steps[-1] < m:
+        sample_steps.append(min(m, (sample_steps[-1] // every + 1) * every))
+    times = [k * tau for k in sample_steps]
     series: dict[str, list[float]] = {n: [] for n in names}
+    from .models import MeanDiagnostics
 
-    def host_states():
-        host = state[0].cpu().numpy()
-        return {n: host[i].copy() for i, n in enumerate(names)}
+    dev_diag = diagnostics if isinstance(diagnostics, MeanDiagnostics) else None
+    host_diag = diagnostics if dev_diag is None else None
+    sampler = _HostSampler(state, first_bad, names) if (host_diag is not None or sample_hook is not None) else None
+    means = dev_diag.device_means(names, 1) if dev_diag is not None else None
+    means_dev = (torch.empty((len(sample_steps), len(comps)), dtype=torch.float64, device="cuda")
+                 if means is not None else None)
 
-    def take_sample(step):
-        t = step * tau
-        times.append(t)
-        if diagnostics is None and sample_hook is None:
-            return
-        st = host_states()
-        if diagnostics is not None:
-            for name, value in diagnostics(st).items():
+    def consume(i):
+        st = sampler.finish()
+        if host_diag is not None:
+            for name, value in host_diag(st).items():
                 series[name].append(value)
         if sample_hook is not None:
-            sample_hook(step, t, st)
+            sample_hook(sample_steps[i], times[i], st)
 
-    take_sample(0)
-    step = 0
-    while step < m:
-        nxt = min(m, (step // every + 1) * every)
-        plan.run(state, step, nxt - step, first_bad)
-        bad = first_bad.cpu().numpy()[0]
-        if bad.min() < INT32_MAX:
-            s = int(bad.min())
-            c = int(np.flatnonzero(bad == s)[0])
-            raise DivergenceError(f"component {names[c]!r} diverged at step {s}", step=s)
-        step = nxt
-        if step % every == 0 or step == m:
-            take_sample(step)
+    # Stepping chunks are enqueued ahead: sample i's device means are written
+    # by a kernel, its host copy (hooks / arbitrary diagnostics only) is
+    # snapshotted on the device and downloaded on a side stream while chunk
+    # i+1 runs; the divergence flags travel with it.
+    if means is not None:
+        means.into(state, means_dev[0])
+    if sampler is not None:
+        sampler.stage()
+    for i in range(1, len(sample_steps)):
+        plan.run(state, sample_steps[i - 1], sample_steps[i] - sample_steps[i - 1], first_bad)
+        if means is not None:
+            means.into(state, means_dev[i])
+        if sampler is not None:
+            consume(i - 1)
+            sampler.stage()
+    if sampler is not None:
+        consume(len(sample_steps) - 1)
+    _raise_if_diverged(first_bad.cpu().numpy()[0], names)
+    if means is not None:
+        vals = means_dev.cpu().numpy()
+        for c, n in enumerate(names):
+            series[n] = [float(x) for x in vals[:, c]]
     if as_torch:
         fields = {n: state[0, i].clone() for i, n in enumerate(names)}
     else:
-        fields = host_states()
+        host = state[0].cpu().numpy()
+        fields = {n: host[i].copy() for i, n in enumerate(names)}
     return RunResult(fields=fields, times=times, series=series, steps=m, tau=tau)

@@ -369,3 +369,145 @@ def build_system(spec, dims: dict, seed: int, overrides=None) -> CoupledSystem:
                  _component(spec, "r", surf(1.0), init), _component(spec, "s", surf(p["epsilon"]), init)]
         kin = BulkSurfaceCoupling("cylinder", {k: p[k] for k in BULK_SURFACE_PARAMS["cylinder"]}, h=float(z.h))
     return CoupledSystem(spec=spec, components=comps, kinetics=kin, equilibrium=eq)
+
+
+# ---------------------------------------------------------------------------
+# diagnostics (models.py:669-755); evaluated on the device by run_simulation /
+# run_ensemble (cg_weighted_sums), on the host when called directly
+# ---------------------------------------------------------------------------
+
+
+def _clipped_widths(grid: np.ndarray, h: float, lo: float, hi: float) -> np.ndarray:
+    """models.py:669-672."""
+    left = np.clip(grid - h / 2.0, lo, hi)
+    right = np.clip(grid + h / 2.0, lo, hi)
+    return right - left
+
+
+def _kind_name(op) -> str:
+    k = getattr(op, "kind", None)
+    return getattr(k, "value", k)
+
+
+def quadrature_weights(cops, normalized: bool = True, rho_star: float | None = None) -> np.ndarray:
+    """Node-centred quadrature weights with the coordinate Jacobian
+    (models.py:675-715): truncated cells at the boundaries, normalised so the
+    mean of a constant is exact.  Host setup, computed once per component."""
+    g = getattr(cops.geometry, "value", cops.geometry)
+    if g == "sphere":
+        theta, phi = cops.theta, cops.phi
+        radius = 1.0 if rho_star is None else rho_star
+        wphi = _clipped_widths(phi.grid, phi.h, 0.0, np.pi)
+        w = np.multiply.outer(np.full(theta.n, theta.h), radius**2 * np.sin(phi.grid) * wphi)
+    else:
+        rho = cops.rho
+        edge = rho.grid[-1] + rho.h if _kind_name(rho) == "lambda" else rho.grid[-1]
+        wrho = _clipped_widths(rho.grid, rho.h, 0.0, edge)
+        theta_w = np.full(cops.theta.n, cops.theta.h)
+        if g == "disk":
+            w = np.multiply.outer(rho.grid * wrho, theta_w)
+        elif g == "ball":
+            phi = cops.phi
+            wphi = _clipped_widths(phi.grid, phi.h, 0.0, np.pi)
+            w = np.multiply.outer(np.multiply.outer(rho.grid**2 * wrho, theta_w), np.sin(phi.grid) * wphi)
+        else:
+            zop = cops.z
+            wz = _clipped_widths(zop.grid, zop.h, 0.0, zop.grid[-1] + zop.h)
+            w = np.multiply.outer(np.multiply.outer(rho.grid * wrho, theta_w), wz)
+    return w / np.sum(w) if normalized else w
+
+
+def integral_mean(field_values: np.ndarray, cops, rho_star: float | None = None) -> float:
+    """Domain-averaged field value (models.py:718-725)."""
+    w = quadrature_weights(cops, normalized=True, rho_star=rho_star)
+    if np.shape(field_values) != w.shape:
+        raise ValueError(f"field shape {np.shape(field_values)} does not match {w.shape}")
+    return float(np.sum(field_values * w))
+
+
+class MeanDiagnostics:
+    """The closure of ``mean_diagnostics`` (models.py:728-744) as an object:
+    called with a dict of host states it returns the physical integral mean
+    of every component (the reference's behaviour); ``run_simulation`` and
+    ``run_ensemble`` recognise it and evaluate it on the device instead, one
+    weighted sum per component and sample (cg_weighted_sums), copying only
+    the scalars back to the host."""
+
+    def __init__(self, names, weights, lifts):
+        self.names = list(names)
+        self.weights = {n: np.ascontiguousarray(weights[n], dtype=np.float64) for n in self.names}
+        self.lifts = {n: float(lifts[n]) for n in self.names}
+
+    def __call__(self, states: dict) -> dict:
+        return {name: float(np.sum(W * self.weights[name])) + self.lifts[name] for name, W in states.items()}
+
+    def device_means(self, names, batch: int = 1) -> DeviceMeans:
+        if list(names) != self.names:
+            raise ValueError(f"diagnostics components {self.names} do not match the system's {list(names)}")
+        return DeviceMeans([self.weights[n] for n in self.names], [self.lifts[n] for n in self.names], batch)
+
+
+def mean_diagnostics(system) -> MeanDiagnostics:
+    """models.py:728-744: quadrature weights built once, lifts restored."""
+    spec = getattr(system, "spec", None)
+    sizes = getattr(spec, "sizes", None) or {}
+    rho_star = sizes.get("rho_star")
+    names = [c.name for c in system.components]
+    return MeanDiagnostics(
+        names,
+        {c.name: quadrature_weights(c.ops, normalized=True, rho_star=rho_star) for c in system.components},
+        {c.name: getattr(c, "lift", 0.0) for c in system.components},
+    )
+
+
+class DeviceMeans:
+    """Integral means of a device state [B][C][...]: out[b, c] =
+    sum(W[b, c] * w[c]) + lift[c] by cg_weighted_sums (fixed summation order,
+    graph-capturable, no host synchronisation)."""
+
+    def __init__(self, weights, lifts, batch: int = 1):
+        import torch
+
+        self.C = len(weights)
+        self.npts = int(np.asarray(weights[0]).size)
+        if any(np.asarray(w).size != self.npts for w in weights):
+            raise ValueError("every component needs weights of the same size")
+        self.B = int(batch)
+        self.w = torch.from_numpy(np.ascontiguousarray(np.stack([np.asarray(w, dtype=np.float64).ravel()
+                                                                  for w in weights]))).to("cuda")
+        self.off = torch.tensor([float(x) for x in lifts], dtype=torch.float64, device="cuda")
+        L = _native.lib()
+        n = L.cg_weighted_sums_scratch(self.B * self.C, self.npts)
+        self.scratch = torch.empty(max(int(n), 1), dtype=torch.float64, device="cuda")
+
+    def into(self, state, out) -> None:
+        """Write the [B, C] means of ``state`` into the device tensor ``out``."""
+        import torch
+
+        if state.dtype != torch.float64 or not state.is_cuda or not state.is_contiguous():
+            raise ValueError("state must be a contiguous float64 CUDA tensor")
+        if state.numel() != self.B * self.C * self.npts:
+            raise ValueError(f"state has {state.numel()} values, expected {self.B * self.C * self.npts}")
+        if out.numel() != self.B * self.C or not out.is_contiguous() or out.dtype != torch.float64:
+            raise ValueError("out must be a contiguous float64 tensor of B*C values")
+        L = _native.lib()
+        _native.check(L.cg_weighted_sums(state.data_ptr(), self.B * self.C, self.npts, self.w.data_ptr(), self.C,
+                                         self.off.data_ptr(), out.data_ptr(), self.scratch.data_ptr(),
+                                         self.scratch.numel(), torch.cuda.current_stream().cuda_stream),
+                      "cg_weighted_sums")
+
+    def __call__(self, state):
+        import torch
+
+        out = torch.empty((self.B, self.C), dtype=torch.float64, device="cuda")
+        self.into(state, out)
+        return out
+
+
+def is_stabilized(times, values, rel: float = 1e-3, abs_tol: float = 1e-6) -> bool:
+    """models.py:747-755."""
+    times = np.asarray(times, dtype=float)
+    values = np.asarray(values, dtype=float)
+    t_star = times[-1]
+    idx = int(np.argmin(np.abs(times - 0.9 * t_star)))
+    return abs(values[-1] - values[idx]) <= rel * abs(values[-1]) + abs_tol

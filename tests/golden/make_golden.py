@@ -13,6 +13,10 @@ Outputs (committed; small):
   full.npz         the five BASELINE configs at FULL size: IC checksums and
                    strided samples / norms of the physical fields after
                    step 1 and step 100 (config 5: members 0, 255, 511)
+  diagnostics.npz  quadrature_weights for every geometry / radial kind and
+                   run_simulation(..., record_every, diagnostics=
+                   mean_diagnostics(system)) series of the five BASELINE
+                   configs at reduced grids
   bulk_surface.npz the two bulk-surface models (models.py:570-661) through
                    model_spec/build_system/run_simulation: small grids in
                    full (IC, kinetics at the IC, state after 20 steps) and
@@ -375,8 +379,37 @@ def make_bulk_surface():
     np.savez_compressed(HERE / "bulk_surface.npz", **d)
 
 
+DIAG_RUNS = {1: (23, 5), 2: (17, 4), 3: (9, 3), 4: (11, 4), 5: (20, 6)}  # (m, record_every)
+
+
+def make_diagnostics():
+    d = {}
+    cases = {
+        "disk": ComponentOps(Geometry.DISK, 1.0, rho=op.build_rho(2, 16, 1.0), theta=op.build_theta(32)),
+        "disk_r2": ComponentOps(Geometry.DISK, 1.0, rho=op.build_rho(2, 9, 2.0), theta=op.build_theta(7)),
+        "sphere": ComponentOps(Geometry.SPHERE, 1.0, theta=op.build_theta(12), phi=op.build_phi_op(9)[0]),
+        "ball": ComponentOps(Geometry.BALL, 1.0, rho=op.build_rho(3, 10, 1.0), theta=op.build_theta(12),
+                             phi=op.build_phi_op(10)[0]),
+        "cylinder": ComponentOps(Geometry.CYLINDER, 1.0, rho=op.build_rho(2, 8, 1.0), theta=op.build_theta(16),
+                                 z=op.build_z(16, 2.0)),
+        "anomalous": ref_member(3, (16, 32)).components[0].ops,
+    }
+    for name, cops in cases.items():
+        d[f"w_{name}"] = models.quadrature_weights(cops, normalized=True)
+        d[f"wu_{name}"] = models.quadrature_weights(cops, normalized=False)
+    d["wu_sphere_r"] = models.quadrature_weights(cases["sphere"], normalized=False, rho_star=1.1653)
+    for k, (m, every) in DIAG_RUNS.items():
+        sysm = ref_config(k, SMALL[k]) if k < 5 else ref_member(7, SMALL[5])
+        t = STEPS[k][1] / STEPS[k][0] * m
+        res = run_simulation(sysm, m, t, record_every=every, diagnostics=models.mean_diagnostics(sysm))
+        d[f"c{k}_times"] = np.array(res.times)
+        for c in sysm.components:
+            d[f"c{k}_{c.name}_series"] = np.array(res.series[c.name])
+    np.savez_compressed(HERE / "diagnostics.npz", **d)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "setup", "steps", "runs", "full", "bulk_surface"]
+    which = sys.argv[1:] or ["rng", "setup", "steps", "runs", "full", "bulk_surface", "diagnostics"]
     for w in which:
         t0 = time.time()
         globals()[f"make_{w}"]()
