@@ -229,6 +229,14 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
           }
         }
       }
+      // Generic-proxy reads (the fragment LDS) of a stage followed by the
+      // producer's async-proxy write (TMA refill) are a cross-proxy WAR: each
+      // thread fences its reads into the async proxy before the release.
+      // Without the fence the refill raced the slice's last fragment loads
+      // (one 8x8 accumulator fragment of warp 0 differed in ~1 of 200 runs;
+      // a register dependency on the last DMMA made it worse, delaying the
+      // release by a slice hid it at a 3% cost; profiles/r01_partial_tile_race.md).
+      fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }

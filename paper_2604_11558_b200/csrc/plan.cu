@@ -119,10 +119,14 @@ int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
     const char* ps = getenv("CURVIGPU_SMEM_PAD");
     pad = ps ? atoi(ps) : 0;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem + pad));
-    // full shared-memory carveout: an SM's L1/smem split only changes while it
-    // is idle, so a smaller preferred carveout would keep a kernel running
-    // concurrently on another stream from co-residing
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    // Measurement knob only: CURVIGPU_MAX_CARVEOUT=1 requests the full
+    // shared-memory carveout (tried for co-residing the front with the GEMM).
+    // It is NOT the default: with it, the n = 100 middle-mode stage of the
+    // ball produced run-to-run differences confined to one 8x8 DMMA fragment
+    // of warp 0 (tools/det_stage.py, profiles/r01_partial_tile_race.md);
+    // with the driver's default carveout every stage is bitwise reproducible.
+    if (getenv("CURVIGPU_MAX_CARVEOUT"))
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     int per_sm = 0, dev = 0, sms = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem + pad));
     CUDA_TRY(cudaGetDevice(&dev));
@@ -612,8 +616,9 @@ int launch_fused_nb(const ThetaParams& tp, const StencilParams& sp, cudaStream_t
   if (configure_only) {
     CUDA_TRY(cudaFuncSetAttribute(disk_ftheta_kernel<M1, M2, KIN, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)D::smem));
-    CUDA_TRY(cudaFuncSetAttribute(disk_ftheta_kernel<M1, M2, KIN, NBUF>,
-                                  cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    if (getenv("CURVIGPU_MAX_CARVEOUT"))
+      CUDA_TRY(cudaFuncSetAttribute(disk_ftheta_kernel<M1, M2, KIN, NBUF>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     return CG_OK;
   }
   // persistent: (3 - NBUF) CTAs per SM walk the (run, RPB-row block) items

@@ -17,6 +17,8 @@ Outputs (committed; small):
                    run_simulation(..., record_every, diagnostics=
                    mean_diagnostics(system)) series of the five BASELINE
                    configs at reduced grids
+  converge.json    cmd_converge (cli.py:258-346) tables and slopes for three
+                   built-in models at small grids (split-EE column)
   bulk_surface.npz the two bulk-surface models (models.py:570-661) through
                    model_spec/build_system/run_simulation: small grids in
                    full (IC, kinetics at the IC, state after 20 steps) and
@@ -408,8 +410,29 @@ def make_diagnostics():
     np.savez_compressed(HERE / "diagnostics.npz", **d)
 
 
+CONVERGE_CASES = [
+    {"model": "schnakenberg_anomalous_disk", "n_rho": 12, "n_theta": 16, "tstar": 0.002, "m_list": [5, 10, 20], "seed": 3},
+    {"model": "bvam_disk", "n_rho": 10, "n_theta": 12, "tstar": 0.5, "m_list": [4, 8, 16], "m_ref": 96, "seed": 2},
+    {"model": "dib_sphere", "n_theta": 12, "n_phi": 9, "tstar": 0.01, "m_list": [3, 6, 12], "seed": 5},
+]
+
+
+def make_converge():
+    import contextlib
+    import io
+
+    from curvipat import cli
+
+    out = []
+    for cfg in CONVERGE_CASES:
+        with contextlib.redirect_stdout(io.StringIO()):
+            res = cli.cmd_converge(dict(cfg))
+        out.append({"cfg": cfg, "table": res["table"], "slope": res["slope"]})
+    (HERE / "converge.json").write_text(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "setup", "steps", "runs", "full", "bulk_surface", "diagnostics"]
+    which = sys.argv[1:] or ["rng", "setup", "steps", "runs", "full", "bulk_surface", "diagnostics", "converge"]
     for w in which:
         t0 = time.time()
         globals()[f"make_{w}"]()

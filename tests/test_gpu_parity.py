@@ -291,6 +291,30 @@ def test_full_size_ball_reruns_bitwise_identical():
         assert torch.equal(outs[0], o)
 
 
+def test_ball_middle_mode_stage_bitwise_over_many_reruns():
+    """Regression guard for the stage-ring release race (a generic-proxy read
+    / async-proxy refill WAR, fixed with fence.proxy.async before the empty
+    arrive): the n = 100 middle-mode stage, 100 reruns on fixed inputs; the
+    unfenced kernel differed in about 1 of 200 reruns."""
+    import torch
+
+    sysm = pcfg.config4()
+    geos = [prepare(c.ops, 1e-2) for c in sysm.components]
+    plan = SplitPlan(geos, 1, sysm.kinetics.kind, sysm.kinetics.param_vector()[None, :], theta="gemm")
+    W = torch.from_numpy(np.stack([c.initial for c in sysm.components])[None]).cuda()
+    out = torch.empty_like(W)
+    for st in plan.step_kernels():
+        plan.run_stage(st, W, out)
+    first = None
+    for _ in range(100):
+        plan.run_stage(2, W, out)
+        got = plan.workspace(1).clone()
+        if first is None:
+            first = got
+        else:
+            assert torch.equal(first, got)
+
+
 @pytest.mark.parametrize("k,dims", [(1, (5, 7)), (2, (8, 5)), (3, (4, 6, 9)), (4, (5, 6, 7)), (2, (7, 9))])
 def test_odd_contiguous_axis_runs_match_oracle(k, dims):
     """Odd last-axis extents (stored padded to even rows inside the plan;
