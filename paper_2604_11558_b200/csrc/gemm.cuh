@@ -58,7 +58,7 @@ struct StageBytes {
 
 template <int BM, int BN, int STAGES>
 constexpr int gemm_smem_bytes() {
-  return STAGES * StageBytes<BM, BN>::total + StageBytes<BM, BN>::epi + (2 * STAGES + 2) * 8 + 1024;
+  return STAGES * StageBytes<BM, BN>::total + StageBytes<BM, BN>::epi + (2 * STAGES + 4) * 8 + 1024;
 }
 
 // Row permutation within an 8-row group used by the TN fragments: rows of a
@@ -69,7 +69,15 @@ __device__ __forceinline__ int perm8(int g) { return ((g & 3) << 1) | (g >> 2); 
 // mapO: output, both viewed as (N, M, slab, field) with a (BN, BM) box; the
 // epilogue tile goes through shared memory: W arrives by TMA during the
 // mainloop, results leave by a bulk tensor store.
-template <int VAR, int BM, int BN, int WM, int WN, int STAGES, int EPI, int MINB>
+//
+// KS > 1 (small problems, fewer tiles than SMs): split-K over a cluster of KS
+// CTAs.  Cluster rank r runs k slices [r KT / KS, (r+1) KT / KS) of every tile
+// of the cluster; ranks 1.. write their partial accumulators into their own
+// etile, rank 0 pulls them over DSMEM (ld.shared::cluster) and adds them in
+// rank order -- a fixed summation order, so results stay bitwise
+// reproducible -- then runs the epilogue alone.  Handshakes are mbarriers
+// armed across the cluster (red_full in rank 0, red_empty in each peer).
+template <int VAR, int BM, int BN, int WM, int WN, int STAGES, int EPI, int MINB, int KS = 1>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
     gemm_f64_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                     const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapO,
@@ -90,10 +98,20 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
   uint64_t* empty = full + STAGES;
   uint64_t* epi_full = empty + STAGES;   // W tile landed (axpy)
   uint64_t* epi_empty = epi_full + 1;    // previous tile's store has read etile
+  uint64_t* red_full = epi_empty + 1;    // KS > 1, rank 0: the peers' partials are in their etiles
+  uint64_t* red_empty = red_full + 1;    // KS > 1, peers: rank 0 has read this CTA's partial
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KT = (p.K + 15) >> 4;
   const int ntiles = p.nbatch * p.tiles_m * p.tiles_n;
+  int rank = 0, cid = blockIdx.x, ncl = gridDim.x, kt_begin = 0, kt_end = KT;
+  if constexpr (KS > 1) {
+    rank = (int)cluster_ctarank();
+    cid = blockIdx.x / KS;
+    ncl = gridDim.x / KS;
+    kt_begin = rank * KT / KS;
+    kt_end = (rank + 1) * KT / KS;
+  }
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -102,9 +120,16 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
     }
     mbar_init(epi_full, 1);
     mbar_init(epi_empty, 1);
+    if constexpr (KS > 1) {
+      mbar_init(red_full, (KS - 1) * NCW);
+      mbar_init(red_empty, NCW);
+    }
     fence_barrier_init();
   }
-  __syncthreads();
+  if (KS > 1)
+    cluster_sync_all();  // barrier inits visible to the peers before any remote arrive
+  else
+    __syncthreads();
 
   // Persistent static schedule: CTA b takes tiles b, b + grid, ...; tile ->
   // (batch item, m tile, n tile) with n fastest so neighbouring CTAs share the
@@ -117,7 +142,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
       tma_prefetch_desc(&mapA);
       tma_prefetch_desc(&mapB);
       int it = 0, tc = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tc) {
+      for (int tile = KS > 1 ? cid : (int)blockIdx.x; tile < ntiles; tile += KS > 1 ? ncl : (int)gridDim.x, ++tc) {
         int r = tile;
         const int tn = r % p.tiles_n;
         r /= p.tiles_n;
@@ -126,7 +151,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
         const int f = t / p.nslab, s = t - f * p.nslab;
         const int c = f % p.ncomp;
         const int m0 = tm * BM, n0 = tn * BN;
-        for (int kt = 0; kt < KT; ++kt, ++it) {
+        for (int kt = KS > 1 ? kt_begin : 0; kt < (KS > 1 ? kt_end : KT); ++kt, ++it) {
           const int st = it % STAGES;
           if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
           uint8_t* sa = smem + st * STAGE;
@@ -142,13 +167,17 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
             for (int q = 0; q < BN / 16; ++q) tma_load_4d(sb + q * 2048, &mapB, &full[st], n0 + 16 * q, kt * 16, s, f);
           }
         }
-        if (EPI == EPI_AXPY) {
+        if (EPI == EPI_AXPY && rank == 0) {
           // W tile for this tile's epilogue, once the previous tile's store has drained etile
           if (tc > 0) mbar_wait(epi_empty, (tc - 1) & 1);
           mbar_arrive_expect_tx(epi_full, EPIB);
           tma_load_4d(etile, &mapW, epi_full, n0, m0, s, f);
         }
       }
+    }
+    if (KS > 1) {
+      __syncwarp();
+      cluster_sync_all();  // no CTA leaves while a peer may still touch its shared memory
     }
     return;
   }
@@ -161,7 +190,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
   if (EPI == EPI_AXPY) step_now = *p.step;
   int it = 0, tc = 0;
 
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tc) {
+  for (int tile = KS > 1 ? cid : (int)blockIdx.x; tile < ntiles; tile += KS > 1 ? ncl : (int)gridDim.x, ++tc) {
     int r = tile;
     const int tn = r % p.tiles_n;
     r /= p.tiles_n;
@@ -177,7 +206,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
 #pragma unroll
       for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    for (int kt = 0; kt < KT; ++kt, ++it) {
+    for (int kt = KS > 1 ? kt_begin : 0; kt < (KS > 1 ? kt_end : KT); ++kt, ++it) {
       const int st = it % STAGES;
       mbar_wait(&full[st], (it / STAGES) & 1);
       // mma.sync.aligned needs the whole warp converged: lanes leave the
@@ -239,6 +268,44 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
+    }
+
+    if (KS > 1) {
+      // ---------------- split-K reduction over DSMEM (fixed rank order) ----------------
+      // partial layout [warp][i][j][lane] (double2): lane-contiguous 16-byte accesses
+      const uint32_t etile_s = smem_u32(etile);
+      if (rank != 0) {
+        if (tc > 0) mbar_wait_cluster(red_empty, (tc - 1) & 1);  // rank 0 has read the previous partial
+        __syncwarp();
+        double2* part = reinterpret_cast<double2*>(etile);
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j)
+            part[((warp * MT + i) * NT + j) * 32 + lane] = make_double2(acc[i][j][0], acc[i][j][1]);
+        fence_acq_rel_cluster();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(red_full), 0));
+        continue;  // rank 0 runs the epilogue
+      }
+      mbar_wait_cluster(red_full, tc & 1);
+      __syncwarp();
+#pragma unroll 1
+      for (int q = 1; q < KS; ++q) {
+        const uint32_t peer = mapa_shared(etile_s, (uint32_t)q);
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const double2 v = ld_shared_cluster_f64x2(peer + 16u * (((warp * MT + i) * NT + j) * 32 + lane));
+            acc[i][j][0] += v.x;
+            acc[i][j][1] += v.y;
+          }
+      }
+      fence_acq_rel_cluster();
+      __syncwarp();
+      if (lane == 0)
+        for (int q = 1; q < KS; ++q) mbar_arrive_cluster(mapa_shared(smem_u32(red_empty), (uint32_t)q));
     }
 
     // ---------------- fused epilogue through the shared-memory tile ----------------
@@ -348,6 +415,10 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
     }
   }
   if (threadIdx.x == 0) bulk_wait0();
+  if (KS > 1) {
+    __syncwarp();
+    cluster_sync_all();
+  }
 }
 
 }  // namespace cg

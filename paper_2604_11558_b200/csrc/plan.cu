@@ -91,8 +91,10 @@ int make_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
 struct TileCfg {
   int BM, BN;
 };
-constexpr int kNumCfg = 7;
-constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {64, 128}, {128, 128}, {64, 64}};
+constexpr int kNumCfg = 9;
+// 7, 8: the 64x64 configuration split-K over clusters of 2 / 4 CTAs
+constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {64, 128}, {128, 128}, {64, 64},
+                                    {64, 64}, {64, 64}};
 
 // BM, BN, warp tile, stages; 32x32 warp tiles keep the accumulators +
 // fragments under ~160 registers without spills.
@@ -106,42 +108,75 @@ constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {
 #define CFG6 64, 64, 32, 32, 6, 3
 
 // configure_only: set the dynamic shared memory opt-in (done at plan
-// creation, never inside a stream capture).
-template <int VAR, int BM, int BN, int WM, int WN, int ST, int MINB, int EPI>
+// creation, never inside a stream capture).  KS > 1 launches clusters of KS
+// CTAs that split each tile's k range (gemm.cuh).
+template <int VAR, int BM, int BN, int WM, int WN, int ST, int MINB, int EPI, int KS = 1>
 int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mw, const CUtensorMap& mo,
                   const GemmParams& p, cudaStream_t stream, bool configure_only) {
-  auto kern = gemm_f64_kernel<VAR, BM, BN, WM, WN, ST, EPI, MINB>;
+  auto kern = gemm_f64_kernel<VAR, BM, BN, WM, WN, ST, EPI, MINB, KS>;
   constexpr int smem = gemm_smem_bytes<BM, BN, ST>();
   constexpr int threads = (BM / WM) * (BN / WN) * 32 + 32;
-  static int resident = 0;  // CTAs of this instantiation that fit on the chip at once
+  static int resident = 0;  // CTAs (KS = 1) or clusters (KS > 1) of this instantiation that fit at once
   static int pad = 0;  // debugging: CURVIGPU_SMEM_PAD extra bytes per CTA (lowers occupancy)
   if (configure_only) {
     const char* ps = getenv("CURVIGPU_SMEM_PAD");
     pad = ps ? atoi(ps) : 0;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem + pad));
     // Measurement knob only: CURVIGPU_MAX_CARVEOUT=1 requests the full
-    // shared-memory carveout (tried for co-residing the front with the GEMM).
-    // It is NOT the default: with it, the n = 100 middle-mode stage of the
-    // ball produced run-to-run differences confined to one 8x8 DMMA fragment
-    // of warp 0 (tools/det_stage.py, profiles/r01_partial_tile_race.md);
-    // with the driver's default carveout every stage is bitwise reproducible.
+    // shared-memory carveout (tried for co-residing the front with the GEMM;
+    // it made the stage-ring race of profiles/r01_partial_tile_race.md, since
+    // fixed, far more frequent).
     if (getenv("CURVIGPU_MAX_CARVEOUT"))
       CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
-    int per_sm = 0, dev = 0, sms = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem + pad));
+    int dev = 0, sms = 0;
     CUDA_TRY(cudaGetDevice(&dev));
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    if (const char* cap = getenv("CURVIGPU_GEMM_CPS")) per_sm = std::min(per_sm, std::max(1, atoi(cap)));
-    resident = (per_sm > 0 ? per_sm : 1) * sms;
+    if (KS == 1) {
+      int per_sm = 0;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem + pad));
+      if (const char* cap = getenv("CURVIGPU_GEMM_CPS")) per_sm = std::min(per_sm, std::max(1, atoi(cap)));
+      resident = (per_sm > 0 ? per_sm : 1) * sms;
+    } else {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = KS;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(KS * sms, 1, 1);
+      cfg.blockDim = dim3(threads, 1, 1);
+      cfg.dynamicSmemBytes = smem + pad;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      CUDA_TRY(cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg));
+      resident = ncl > 0 ? ncl : 1;
+    }
     return CG_OK;
   }
   const long long tiles = (long long)p.nbatch * p.tiles_m * p.tiles_n;
   if (tiles <= 0) return CG_OK;
   if (tiles > INT_MAX) return fail(CG_EUNSUPPORTED, "grid too large");
-  // persistent grid: at most one wave of resident CTAs, each looping over tiles
-  long long blocks = (resident > 0 && tiles > resident) ? resident : tiles;
-  if (getenv("CURVIGPU_NOPERSIST")) blocks = tiles;
-  kern<<<(unsigned)blocks, threads, smem + pad, stream>>>(ma, mb, mw, mo, p);
+  // persistent grid: at most one wave of resident CTAs (clusters), each looping over tiles
+  long long units = (resident > 0 && tiles > resident) ? resident : tiles;
+  if (getenv("CURVIGPU_NOPERSIST")) units = tiles;
+  if (KS == 1) {
+    kern<<<(unsigned)units, threads, smem + pad, stream>>>(ma, mb, mw, mo, p);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = KS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(units * KS), 1, 1);
+    cfg.blockDim = dim3(threads, 1, 1);
+    cfg.dynamicSmemBytes = smem + pad;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, mw, mo, p));
+  }
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
 }
@@ -159,6 +194,8 @@ int launch_gemm_cfg(int cfg, const Maps& m, const GemmParams& p, cudaStream_t st
     case 3: return launch_gemm_t<VAR, CFG3, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
     case 4: return launch_gemm_t<VAR, CFG4, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
     case 5: return launch_gemm_t<VAR, CFG5, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case 7: return launch_gemm_t<VAR, CFG2, EPI, 2>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case 8: return launch_gemm_t<VAR, CFG2, EPI, 4>(m.a, m.b, m.w, m.o, p, stream, conf);
     default: return launch_gemm_t<VAR, CFG6, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
   }
 }
@@ -336,7 +373,7 @@ int upload_operator(cg_plan* p, int var, int n, Get get, double** out, CUtensorM
   return make_map(map, *out, 3, dims, strides, box);
 }
 
-int pick_cfg(int var, long long nbatch, int M, int N, int stage_index) {
+int pick_cfg(int var, long long nbatch, int M, int N, int K, int stage_index) {
   // measurement override: CURVIGPU_TILE_CFG=<cfg> or "<s0>,<s1>,..." per stage
   if (const char* env = getenv("CURVIGPU_TILE_CFG")) {
     int vals[16], nv = 0;
@@ -351,11 +388,26 @@ int pick_cfg(int var, long long nbatch, int M, int N, int stage_index) {
   // Measured on B200 with the TMA epilogue (tools/sweep_tiles.py,
   // profiles/r01_tile_sweep_tmaepi.txt): 64x64 tiles, 4-stage ring, 2 CTAs/SM
   // is the best or within 2% of the best for every stage of every BASELINE
-  // config (larger epilogue tiles cost occupancy).
+  // config (larger epilogue tiles cost occupancy).  Stages with too few tiles
+  // to fill the chip split each tile's k range over a cluster of 2 CTAs when
+  // every rank keeps >= 4 k slices (tools/small_gemm_sweep.py,
+  // profiles/r01_splitk_sweep.jsonl: the sphere's 64-tile stages 13.7 -> 10.9
+  // us; 4-CTA clusters and splits of short k ranges lose to the DSMEM
+  // reduction and cluster handshakes; cfg 8 = 4-CTA clusters stays selectable
+  // through CURVIGPU_TILE_CFG for measurement).
   (void)var;
-  (void)nbatch;
-  (void)M;
-  (void)N;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                  cudaSuccess)
+      sms = 148;
+  }
+  const long long tiles = nbatch * ((M + 63) / 64) * ((N + 63) / 64);
+  const int KT = (K + 15) / 16;
+  if (!getenv("CURVIGPU_NO_SPLITK")) {
+    if (tiles * 2 <= 2LL * sms && KT >= 8) return 7;
+  }
   return 2;
 }
 
@@ -380,7 +432,7 @@ int add_stage(cg_plan* p, int var, int epi, int M, int N, int K, int nslab, int 
     st.ldr = st.N;
   }
   const long long nbatch = (long long)p->B * p->C * nslab;
-  st.cfg = pick_cfg(var, nbatch, M, N, (int)p->stages.size());
+  st.cfg = pick_cfg(var, nbatch, M, N, K, (int)p->stages.size());
   double* op = nullptr;
   const int box_rows = (var == VAR_TN) ? kCfgs[st.cfg].BN : 16;
   int rc = upload_operator(p, var, n_op, get, &op, &st.opmap, box_rows);
