@@ -21,9 +21,9 @@
 
 namespace cg {
 
-template <int M1, int M2, int NBUF = 2>
+template <int M1, int M2, int NBUF = 2, int NT = 256>
 struct FusedDisk {
-  using F = FastTheta<M1, M2>;
+  using F = FastTheta<M1, M2, NT>;
   static constexpr int M = F::M;
   static constexpr int N = 2 * M;         // theta extent
   static constexpr int LPB = F::LPB;      // FFT lines per item
@@ -43,10 +43,11 @@ struct FusedDisk {
 // NBUF = 2: one CTA per SM, item t+2 prefetched into the buffer item t frees.
 // NBUF = 1: two CTAs per SM (register-capped), each refilling its single
 // buffer after its item; the other CTA's arithmetic covers the refill.
-template <int M1, int M2, int KIN, int NBUF>
-__global__ void __launch_bounds__(256, 3 - NBUF) disk_ftheta_kernel(const ThetaParams tp, const StencilParams sp) {
-  using F = FastTheta<M1, M2>;
-  using D = FusedDisk<M1, M2, NBUF>;
+// NT = 64 (small grids): a quarter of the rows per item, four times the items
+template <int M1, int M2, int KIN, int NBUF, int NT = 256>
+__global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kernel(const ThetaParams tp, const StencilParams sp) {
+  using F = FastTheta<M1, M2, NT>;
+  using D = FusedDisk<M1, M2, NBUF, NT>;
   constexpr int M = F::M, TPL = F::TPL, RPB = D::RPB, N = D::N;
   extern __shared__ uint8_t fd_raw[];
   uint8_t* base_s = fd_raw + ((128u - (smem_u32(fd_raw) & 127u)) & 127u);  // stays a shared-space pointer

@@ -327,7 +327,7 @@ struct cg_plan {
   // disk + FFT theta + built-in kinetics: F-build and stages[0] (theta) run
   // as one persistent fused kernel (fused_disk.cuh) inside cg_run
   bool fused_front = false;
-  int fused_m1 = 0, fused_m2 = 0;
+  int fused_m1 = 0, fused_m2 = 0, fused_nt = 256;
 };
 
 namespace {
@@ -567,15 +567,33 @@ int launch_theta(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
   const bool ax = st.epi == EPI_AXPY;
   // register-resident two-phase FFT when the split M = M1*M2 exists and the
   // lines tile the CTA; Stockham smem passes otherwise
-#define TRY_FAST(M1, M2)                                                                   \
-  if (st.N / 2 == (M1) * (M2) && span % FastTheta<M1, M2>::LPB == 0) {                     \
-    const unsigned nb = (unsigned)(lines / FastTheta<M1, M2>::LPB);                        \
-    if (ax)                                                                                \
-      theta_fast_kernel<M1, M2, true><<<nb, 256, FastTheta<M1, M2>::smem, s>>>(tp);        \
-    else                                                                                   \
-      theta_fast_kernel<M1, M2, false><<<nb, 256, FastTheta<M1, M2>::smem, s>>>(tp);       \
-    CUDA_TRY(cudaGetLastError());                                                          \
-    return CG_OK;                                                                          \
+  // 64-thread CTAs when 256-thread ones would leave SMs idle (the sphere's
+  // 512 theta columns: 32 CTAs at 256 threads, 128 at 64)
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const bool small_cta = !getenv("CURVIGPU_NO_SMALL_CTA");
+#define TRY_FAST(M1, M2)                                                                             \
+  if (st.N / 2 == (M1) * (M2) && span % FastTheta<M1, M2>::LPB == 0) {                               \
+    using F64 = FastTheta<M1, M2, 64>;                                                               \
+    if (small_cta && lines / FastTheta<M1, M2>::LPB < sms && span % F64::LPB == 0) {                  \
+      const unsigned nb = (unsigned)(lines / F64::LPB);                                              \
+      if (ax)                                                                                        \
+        theta_fast_kernel<M1, M2, true, 64><<<nb, 64, F64::smem, s>>>(tp);                           \
+      else                                                                                           \
+        theta_fast_kernel<M1, M2, false, 64><<<nb, 64, F64::smem, s>>>(tp);                          \
+    } else {                                                                                         \
+      const unsigned nb = (unsigned)(lines / FastTheta<M1, M2>::LPB);                                \
+      if (ax)                                                                                        \
+        theta_fast_kernel<M1, M2, true><<<nb, 256, FastTheta<M1, M2>::smem, s>>>(tp);                \
+      else                                                                                           \
+        theta_fast_kernel<M1, M2, false><<<nb, 256, FastTheta<M1, M2>::smem, s>>>(tp);               \
+    }                                                                                                \
+    CUDA_TRY(cudaGetLastError());                                                                    \
+    return CG_OK;                                                                                    \
   }
   TRY_FAST(4, 4)
   TRY_FAST(4, 8)
@@ -662,15 +680,14 @@ int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
 }
 
 // Launch one full step: Win (+G) -> F -> stage chain -> Wout.
-template <int M1, int M2, int KIN, int NBUF>
+template <int M1, int M2, int KIN, int NBUF, int NT = 256>
 int launch_fused_nb(const ThetaParams& tp, const StencilParams& sp, cudaStream_t s, bool configure_only) {
-  using D = FusedDisk<M1, M2, NBUF>;
+  using D = FusedDisk<M1, M2, NBUF, NT>;
+  auto kern = disk_ftheta_kernel<M1, M2, KIN, NBUF, NT>;
   if (configure_only) {
-    CUDA_TRY(cudaFuncSetAttribute(disk_ftheta_kernel<M1, M2, KIN, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)D::smem));
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D::smem));
     if (getenv("CURVIGPU_MAX_CARVEOUT"))
-      CUDA_TRY(cudaFuncSetAttribute(disk_ftheta_kernel<M1, M2, KIN, NBUF>,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     return CG_OK;
   }
   // persistent: (3 - NBUF) CTAs per SM walk the (run, RPB-row block) items
@@ -682,28 +699,30 @@ int launch_fused_nb(const ThetaParams& tp, const StencilParams& sp, cudaStream_t
   }
   const long long items = (long long)sp.batch * (sp.n1 / D::RPB);
   static const int cps = getenv("CURVIGPU_FRONT_CPS") ? std::max(1, atoi(getenv("CURVIGPU_FRONT_CPS"))) : 3 - NBUF;
-  const unsigned blocks = (unsigned)std::min<long long>(items, (long long)num_sms * std::min(cps, 3 - NBUF));
-  disk_ftheta_kernel<M1, M2, KIN, NBUF><<<blocks, 256, D::smem, s>>>(tp, sp);
+  const unsigned blocks =
+      (unsigned)std::min<long long>(items, (long long)num_sms * std::min(cps, 3 - NBUF) * (256 / NT));
+  kern<<<blocks, NT, D::smem, s>>>(tp, sp);
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
 }
 
 template <int M1, int M2, int KIN>
-int launch_fused_t(const ThetaParams& tp, const StencilParams& sp, cudaStream_t s, bool configure_only) {
+int launch_fused_t(const ThetaParams& tp, const StencilParams& sp, cudaStream_t s, bool configure_only, int nt) {
   static const int nbuf = getenv("CURVIGPU_FUSED_NBUF") ? atoi(getenv("CURVIGPU_FUSED_NBUF")) : 1;
+  if (nt == 64) return launch_fused_nb<M1, M2, KIN, 1, 64>(tp, sp, s, configure_only);
   if (nbuf == 1) return launch_fused_nb<M1, M2, KIN, 1>(tp, sp, s, configure_only);
   return launch_fused_nb<M1, M2, KIN, 2>(tp, sp, s, configure_only);
 }
 
 template <int M1, int M2>
-int launch_fused_k(int kin, const ThetaParams& tp, const StencilParams& sp, cudaStream_t s, bool conf) {
+int launch_fused_k(int kin, const ThetaParams& tp, const StencilParams& sp, cudaStream_t s, bool conf, int nt) {
   switch (kin) {
-    case KIN_SCHNAKENBERG: return launch_fused_t<M1, M2, KIN_SCHNAKENBERG>(tp, sp, s, conf);
-    case KIN_BRUSSELATOR: return launch_fused_t<M1, M2, KIN_BRUSSELATOR>(tp, sp, s, conf);
-    case KIN_GRAY_SCOTT: return launch_fused_t<M1, M2, KIN_GRAY_SCOTT>(tp, sp, s, conf);
-    case KIN_BVAM_ETA: return launch_fused_t<M1, M2, KIN_BVAM_ETA>(tp, sp, s, conf);
-    case KIN_BVAM: return launch_fused_t<M1, M2, KIN_BVAM>(tp, sp, s, conf);
-    default: return launch_fused_t<M1, M2, KIN_DIB>(tp, sp, s, conf);
+    case KIN_SCHNAKENBERG: return launch_fused_t<M1, M2, KIN_SCHNAKENBERG>(tp, sp, s, conf, nt);
+    case KIN_BRUSSELATOR: return launch_fused_t<M1, M2, KIN_BRUSSELATOR>(tp, sp, s, conf, nt);
+    case KIN_GRAY_SCOTT: return launch_fused_t<M1, M2, KIN_GRAY_SCOTT>(tp, sp, s, conf, nt);
+    case KIN_BVAM_ETA: return launch_fused_t<M1, M2, KIN_BVAM_ETA>(tp, sp, s, conf, nt);
+    case KIN_BVAM: return launch_fused_t<M1, M2, KIN_BVAM>(tp, sp, s, conf, nt);
+    default: return launch_fused_t<M1, M2, KIN_DIB>(tp, sp, s, conf, nt);
   }
 }
 
@@ -740,9 +759,9 @@ int launch_fused_front(cg_plan* p, const double* Win, bool count_step, cudaStrea
   sp.nparams = p->P;
   sp.W = Win;
   sp.step = count_step ? p->step_dev : nullptr;
-  if (p->fused_m1 == 8 && p->fused_m2 == 16) return launch_fused_k<8, 16>(p->kin, tp, sp, s, conf);
-  if (p->fused_m1 == 8 && p->fused_m2 == 8) return launch_fused_k<8, 8>(p->kin, tp, sp, s, conf);
-  return launch_fused_k<4, 8>(p->kin, tp, sp, s, conf);
+  if (p->fused_m1 == 8 && p->fused_m2 == 16) return launch_fused_k<8, 16>(p->kin, tp, sp, s, conf, p->fused_nt);
+  if (p->fused_m1 == 8 && p->fused_m2 == 8) return launch_fused_k<8, 8>(p->kin, tp, sp, s, conf, p->fused_nt);
+  return launch_fused_k<4, 8>(p->kin, tp, sp, s, conf, p->fused_nt);
 }
 
 // Launch one full step: Win (+G) -> F -> stage chain -> Wout.
@@ -788,6 +807,13 @@ int setup_fused_front(cg_plan* p) {
   if (p->n1 % (lpb / 2) != 0) return CG_OK;
   p->fused_m1 = m1;
   p->fused_m2 = m2;
+  // fewer 256-thread items than SMs (config 1: 4): 64-thread items, a
+  // quarter of the rows each
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long items256 = (long long)p->B * (p->n1 / (lpb / 2));
+  if (items256 < sms && p->n1 % (lpb / 8) == 0 && (lpb / 8) % 2 == 0 && !getenv("CURVIGPU_NO_SMALL_CTA"))
+    p->fused_nt = 64;
   int rc = launch_fused_front(p, nullptr, false, nullptr, true);
   if (rc) return rc;
   p->fused_front = true;
@@ -1103,6 +1129,11 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
                             (int)FastTheta<M1, M2>::smem);                                                    \
   e2 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                             (int)FastTheta<M1, M2>::smem);                                                    \
+  if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));  \
+  e1 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                            (int)FastTheta<M1, M2, 64>::smem);                                                \
+  e2 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,\
+                            (int)FastTheta<M1, M2, 64>::smem);                                                \
   if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
     OPT_IN(4, 4)
     OPT_IN(4, 8)

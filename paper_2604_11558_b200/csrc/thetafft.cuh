@@ -341,13 +341,15 @@ __device__ __forceinline__ void dft_reg(double2* a) {
   if constexpr (L > 1) dit_stage<L, 2, INV>(a);
 }
 
-template <int M1, int M2>
+// NT threads per CTA: 256, or 64 for problems with too few lines to give
+// every SM a CTA at 256 (the sphere's 512 theta columns, config 1's disk)
+template <int M1, int M2, int NT = 256>
 struct FastTheta {
   static constexpr int M = M1 * M2;
   // threads per line = min(M1, M2): in each phase every thread runs
   // max/min DFTs, so no lane idles during the heavy phase
   static constexpr int TPL = M1 < M2 ? M1 : M2;
-  static constexpr int LPB = 256 / TPL;          // lines per CTA
+  static constexpr int LPB = NT / TPL;           // lines per CTA
   static constexpr int LDT = M1 * (M2 + 1);      // padded transpose tile (complex)
   static constexpr int SL0 = LDT > M ? LDT : M;
   static constexpr int SL = (SL0 % 2 == 0) ? SL0 + 1 : SL0;  // odd line stride: lines land on distinct banks
@@ -497,9 +499,9 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
   }
 }
 
-template <int M1, int M2, bool AXPY>
-__global__ void __launch_bounds__(256) theta_fast_kernel(const ThetaParams p) {
-  using F = FastTheta<M1, M2>;
+template <int M1, int M2, bool AXPY, int NT = 256>
+__global__ void __launch_bounds__(NT) theta_fast_kernel(const ThetaParams p) {
+  using F = FastTheta<M1, M2, NT>;
   constexpr int M = F::M, TPL = F::TPL, LPB = F::LPB;
   extern __shared__ double2 tf_smem[];
   const int N = 2 * M;
