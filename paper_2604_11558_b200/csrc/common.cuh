@@ -97,6 +97,18 @@ __device__ __forceinline__ void named_bar(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
 
+// ---- programmatic dependent launch (kernels of one step chain) ----
+// A kernel launched with cudaLaunchAttributeProgrammaticStreamSerialization
+// is launched while its predecessor in the stream drains; every such kernel
+// calls pdl_wait() before its first global-memory access to step data (reads
+// or writes), which blocks until the predecessor grid has completed and its
+// writes are visible.  No kernel triggers early (griddepcontrol.
+// launch_dependents): measured on B200 (tools/step_times.py), an early
+// trigger in the persistent kernels let the next grid's CTAs queue onto SMs
+// and cost up to 16 % on the cluster split-K chains, while the implicit
+// trigger at CTA exit keeps the launch-latency saving (config 1 -9 %).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // ---- thread-block clusters (split-K GEMM: partial tiles reduced over DSMEM) ----
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

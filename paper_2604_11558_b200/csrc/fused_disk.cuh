@@ -64,7 +64,6 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
   constexpr int PS = D::PS;  // == tp.phis_ld (checked at plan set-up)
   const uint32_t item_bytes = (uint32_t)(2 * (RPB + 2) * row_bytes + 2 * RPB * PS * sizeof(double));
 
-  if (sp.step && blockIdx.x == 0 && threadIdx.x == 0) *sp.step += 1;
 
   // copies of one item into buffer k (issued by one thread)
   auto issue = [&](int item, int k) {
@@ -98,8 +97,13 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    // twiddles are plan constants: loaded before waiting on the previous kernel
     mbar_arrive_expect_tx(&full[2], (uint32_t)D::twb);
     bulk_load_1d(tw_s, tp.tw, (uint32_t)D::twb, &full[2]);
+  }
+  pdl_wait();
+  if (sp.step && blockIdx.x == 0 && threadIdx.x == 0) *sp.step += 1;
+  if (threadIdx.x == 0) {
     if ((int)blockIdx.x < items) issue(blockIdx.x, 0);
     if (NBUF == 2 && (int)(blockIdx.x + gridDim.x) < items) issue(blockIdx.x + gridDim.x, 1);
   }

@@ -130,6 +130,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
     cluster_sync_all();  // barrier inits visible to the peers before any remote arrive
   else
     __syncthreads();
+  pdl_wait();     // the previous kernel's outputs (X / W / step counter) are complete
 
   // Persistent static schedule: CTA b takes tiles b, b + grid, ...; tile ->
   // (batch item, m tile, n tile) with n fastest so neighbouring CTAs share the

@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "curvigpu.h"
@@ -61,6 +62,31 @@ EncodeTiledFn encode_fn() {
       fn = reinterpret_cast<EncodeTiledFn>(p);
   }
   return fn;
+}
+
+// Launch a step-chain kernel with programmatic dependent launch (common.cuh:
+// every such kernel calls pdl_wait() before touching step data), so its
+// launch and prologue overlap the previous kernel's tail.  CURVIGPU_NO_PDL=1
+// launches plainly (measurement).
+bool pdl_enabled() {
+  static const bool on = getenv("CURVIGPU_NO_PDL") == nullptr;
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+  return CG_OK;
 }
 
 // fp64 tensor map, 128B swizzle, zero fill; dims innermost first, strides in bytes.
@@ -161,20 +187,23 @@ int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   long long units = (resident > 0 && tiles > resident) ? resident : tiles;
   if (getenv("CURVIGPU_NOPERSIST")) units = tiles;
   if (KS == 1) {
-    kern<<<(unsigned)units, threads, smem + pad, stream>>>(ma, mb, mw, mo, p);
+    int rc = launch_pdl(kern, dim3((unsigned)units), dim3(threads), smem + pad, stream, ma, mb, mw, mo, p);
+    if (rc) return rc;
   } else {
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = KS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.gridDim = dim3((unsigned)(units * KS), 1, 1);
     cfg.blockDim = dim3(threads, 1, 1);
     cfg.dynamicSmemBytes = smem + pad;
     cfg.stream = stream;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, mw, mo, p));
   }
   CUDA_TRY(cudaGetLastError());
@@ -240,7 +269,8 @@ int launch_fbuild_t(const StencilParams& p, cudaStream_t s, bool configure_only)
   if (smem > 200 * 1024) return fail(CG_EUNSUPPORTED, "F-build tile exceeds shared memory");
   const dim3 grid((unsigned)((p.n1 + S::RB - 1) / S::RB), S::D3 ? (unsigned)p.n2 : 1u, (unsigned)p.batch);
   const unsigned threads = (unsigned)((nl + 31) / 32 * 32);
-  fbuild_rows_kernel<GEOM, KIN><<<grid, threads, smem, s>>>(p);
+  int rc = launch_pdl(fbuild_rows_kernel<GEOM, KIN>, grid, dim3(threads), smem, s, p);
+  if (rc) return rc;
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
 }
@@ -582,18 +612,13 @@ int launch_theta(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
     if (small_cta && lines / FastTheta<M1, M2>::LPB < sms && span % F64::LPB == 0) {                  \
       const unsigned nb = (unsigned)(lines / F64::LPB);                                              \
       if (ax)                                                                                        \
-        theta_fast_kernel<M1, M2, true, 64><<<nb, 64, F64::smem, s>>>(tp);                           \
-      else                                                                                           \
-        theta_fast_kernel<M1, M2, false, 64><<<nb, 64, F64::smem, s>>>(tp);                          \
-    } else {                                                                                         \
-      const unsigned nb = (unsigned)(lines / FastTheta<M1, M2>::LPB);                                \
-      if (ax)                                                                                        \
-        theta_fast_kernel<M1, M2, true><<<nb, 256, FastTheta<M1, M2>::smem, s>>>(tp);                \
-      else                                                                                           \
-        theta_fast_kernel<M1, M2, false><<<nb, 256, FastTheta<M1, M2>::smem, s>>>(tp);               \
+        return launch_pdl(theta_fast_kernel<M1, M2, true, 64>, dim3(nb), dim3(64), F64::smem, s, tp);  \
+      return launch_pdl(theta_fast_kernel<M1, M2, false, 64>, dim3(nb), dim3(64), F64::smem, s, tp);   \
     }                                                                                                \
-    CUDA_TRY(cudaGetLastError());                                                                    \
-    return CG_OK;                                                                                    \
+    const unsigned nb = (unsigned)(lines / FastTheta<M1, M2>::LPB);                                  \
+    if (ax)                                                                                          \
+      return launch_pdl(theta_fast_kernel<M1, M2, true>, dim3(nb), dim3(256), FastTheta<M1, M2>::smem, s, tp); \
+    return launch_pdl(theta_fast_kernel<M1, M2, false>, dim3(nb), dim3(256), FastTheta<M1, M2>::smem, s, tp); \
   }
   TRY_FAST(4, 4)
   TRY_FAST(4, 8)
@@ -603,12 +628,8 @@ int launch_theta(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
 #undef TRY_FAST
   const unsigned blocks = (unsigned)(lines / tp.W);
   const size_t smem = theta_smem_bytes(st.N, st.tW);
-  if (st.epi == EPI_AXPY)
-    theta_prop_kernel<true><<<blocks, 256, smem, s>>>(tp);
-  else
-    theta_prop_kernel<false><<<blocks, 256, smem, s>>>(tp);
-  CUDA_TRY(cudaGetLastError());
-  return CG_OK;
+  if (st.epi == EPI_AXPY) return launch_pdl(theta_prop_kernel<true>, dim3(blocks), dim3(256), smem, s, tp);
+  return launch_pdl(theta_prop_kernel<false>, dim3(blocks), dim3(256), smem, s, tp);
 }
 
 int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, int* first_bad, cudaStream_t s) {
@@ -701,7 +722,8 @@ int launch_fused_nb(const ThetaParams& tp, const StencilParams& sp, cudaStream_t
   static const int cps = getenv("CURVIGPU_FRONT_CPS") ? std::max(1, atoi(getenv("CURVIGPU_FRONT_CPS"))) : 3 - NBUF;
   const unsigned blocks =
       (unsigned)std::min<long long>(items, (long long)num_sms * std::min(cps, 3 - NBUF) * (256 / NT));
-  kern<<<blocks, NT, D::smem, s>>>(tp, sp);
+  int rc = launch_pdl(kern, dim3(blocks), dim3(NT), D::smem, s, tp, sp);
+  if (rc) return rc;
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
 }

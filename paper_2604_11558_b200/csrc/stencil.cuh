@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
   using S = FbuildShape<GEOM>;
   extern __shared__ double fb_smem[];
   __shared__ RowCoef rcs[8 * S::RB];  // up to 8 components
+  pdl_wait();
   if (p.step && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *p.step += 1;
   const int nl = S::D3 ? p.n3 : p.n2;
   const int n1 = p.n1;

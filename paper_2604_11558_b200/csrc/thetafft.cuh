@@ -135,6 +135,7 @@ __device__ __forceinline__ void fft_lines(double2*& cur, double2*& alt, int M, i
 
 template <bool AXPY>
 __global__ void __launch_bounds__(256) theta_prop_kernel(const ThetaParams p) {
+  pdl_wait();
   extern __shared__ double2 tp_smem[];
   const int N = p.N, M = N / 2, W = p.W, ld = M + 1;
   double2* bufA = tp_smem;
@@ -501,6 +502,7 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
 
 template <int M1, int M2, bool AXPY, int NT = 256>
 __global__ void __launch_bounds__(NT) theta_fast_kernel(const ThetaParams p) {
+  pdl_wait();
   using F = FastTheta<M1, M2, NT>;
   constexpr int M = F::M, TPL = F::TPL, LPB = F::LPB;
   extern __shared__ double2 tf_smem[];
