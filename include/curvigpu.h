@@ -123,6 +123,14 @@ typedef struct {
   const double* kin_params; /* [batch][nparams] */
   const double* lift;     /* [ncomp] constant lift restoring physical values */
   int options;            /* CG_OPT_* bit set */
+  /* 0: one operator set per component, shared by every run (the arrays
+   * above have a leading [ncomp] index).  1: heterogeneous ensemble -- one
+   * operator set per (run, component), leading index [batch * ncomp] in
+   * field order f = run * ncomp + component (coeff, bands, theta stencil,
+   * d_rho, d_phi, the dense transforms and the Phi tensors; lift stays
+   * [ncomp]).  Runs may then differ in diffusion coefficients and domain
+   * sizes as long as the grid extents agree. */
+  int ops_per_run;
 } cg_desc;
 
 /* options: apply the periodic-theta pair Q_theta diag(Phi) Q_theta^T as an

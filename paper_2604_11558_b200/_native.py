@@ -55,6 +55,7 @@ class cg_desc(ctypes.Structure):
         ("kin_params", _dp),
         ("lift", _dp),
         ("options", ctypes.c_int),
+        ("ops_per_run", ctypes.c_int),
     ]
 
 

@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
                    &full[k]);
       if (i0 == 0) bulk_load_1d(dst, src, row_bytes, &full[k]);
       if (i0 + RPB >= n1) bulk_load_1d(dst + (size_t)(RPB + 1) * N, src + (long long)(n1 - 1) * N, row_bytes, &full[k]);
-      bulk_load_1d(phs + (size_t)comp * RPB * PS, tp.phis + ((long long)comp * tp.nclass + i0) * PS,
+      bulk_load_1d(phs + (size_t)comp * RPB * PS, tp.phis + ((long long)(b * sp.opb + comp) * tp.nclass + i0) * PS,
                    (uint32_t)(RPB * PS * sizeof(double)), &full[k]);
     }
   };
@@ -111,7 +111,6 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
   const int tid = threadIdx.x;
   const int ln = tid / TPL, lt = tid - ln * TPL;
   const int comp = ln / RPB, rr = ln - comp * RPB;  // line = (species, interior row)
-  const CompCoef kc = comp_coef<0>(sp, comp, 0, N);
   const double lift0 = sp.lift[0], lift1 = sp.lift[1];
   mbar_wait(&full[2], 0);
   for (int i = threadIdx.x; i < M; i += blockDim.x) twa_s[i] = tw_s[2 * (i % M2) * (i / M2)];
@@ -130,13 +129,15 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
     double kin[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) kin[q] = (q < sp.nparams) ? __ldg(sp.kin + (long long)b * sp.nparams + q) : 0.0;
+    const int oc = b * sp.opb + comp;  // operator set of this (run, species)
+    const CompCoef kc = comp_coef<0>(sp, oc, 0, N);
     RowCoef rc;
     {
-      const double* bands = sp.rho_b + (long long)comp * 3 * n1;
+      const double* bands = sp.rho_b + (long long)oc * 3 * n1;
       rc.a = __ldg(bands + row);
       rc.b = (row < n1 - 1) ? __ldg(bands + n1 + row) : 0.0;
       rc.c = (row > 0) ? __ldg(bands + 2 * n1 + row - 1) : 0.0;
-      rc.d = __ldg(sp.d_rho + comp * n1 + row);
+      rc.d = __ldg(sp.d_rho + (long long)oc * n1 + row);
     }
     mbar_wait(&full[k], NBUF == 2 ? ((t >> 1) & 1) : (t & 1));
 

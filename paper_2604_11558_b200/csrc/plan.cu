@@ -334,6 +334,7 @@ constexpr int kChunk = 16;  // steps per captured graph (even)
 
 struct cg_plan {
   int geom, n1, n2, n3, B, C, kin, P;
+  int NO = 0;  // operator sets: C (shared by the runs) or B * C (heterogeneous ensemble)
   double tau;
   // Storage layout: the contiguous (last) axis of logical extent nl is stored
   // with row stride ld = even(nl) so every TMA row stride is a multiple of 16
@@ -385,8 +386,8 @@ int upload(cg_plan* p, const double* host, size_t count, double** out) {
 template <typename Get>
 int upload_operator(cg_plan* p, int var, int n, Get get, double** out, CUtensorMap* map, int box_rows) {
   const int np = (n + 1) & ~1;
-  std::vector<double> h((size_t)p->C * n * np, 0.0);
-  for (int c = 0; c < p->C; ++c)
+  std::vector<double> h((size_t)p->NO * n * np, 0.0);
+  for (int c = 0; c < p->NO; ++c)
     for (int r = 0; r < n; ++r)
       for (int q = 0; q < n; ++q) {
         // TN: B[n_out = r][k = q] = L[r][q];  NN: A^T[k = q][m = r] = L[r][q]
@@ -397,7 +398,7 @@ int upload_operator(cg_plan* p, int var, int n, Get get, double** out, CUtensorM
       }
   int rc = upload(p, h.data(), h.size(), out);
   if (rc) return rc;
-  const uint64_t dims[3] = {(uint64_t)n, (uint64_t)n, (uint64_t)p->C};
+  const uint64_t dims[3] = {(uint64_t)n, (uint64_t)n, (uint64_t)p->NO};
   const uint64_t strides[2] = {(uint64_t)np * 8, (uint64_t)n * np * 8};
   const uint32_t box[3] = {16, (uint32_t)box_rows, 1};
   return make_map(map, *out, 3, dims, strides, box);
@@ -504,8 +505,8 @@ int add_theta_stage(cg_plan* p, int epi, int src, int dst, int N, int A, int Bc,
   int W = 16;
   while (W > 1 && (span % W != 0 || theta_smem_bytes(N, W) > 96 * 1024)) W /= 2;
   st.tW = W;
-  std::vector<double> h((size_t)p->C * nclass * (M + 1));
-  for (int c = 0; c < p->C; ++c)
+  std::vector<double> h((size_t)p->NO * nclass * (M + 1));
+  for (int c = 0; c < p->NO; ++c)
     for (int cls = 0; cls < nclass; ++cls)
       for (int j = 0; j <= M; ++j) {
         const int col = (j == 0) ? 0 : (j == M ? N - 1 : 2 * j - 1);
@@ -517,8 +518,8 @@ int add_theta_stage(cg_plan* p, int epi, int src, int dst, int N, int A, int Bc,
   // scaled copy for the register FFT kernels: exact power-of-two factors
   // (1/(2M) at j = 0, M; 1/(4M) otherwise), rows padded to an odd multiple of 8
   const int ps = phis_stride(M);
-  std::vector<double> hs((size_t)p->C * nclass * ps, 0.0);
-  for (size_t r = 0; r < (size_t)p->C * nclass; ++r)
+  std::vector<double> hs((size_t)p->NO * nclass * ps, 0.0);
+  for (size_t r = 0; r < (size_t)p->NO * nclass; ++r)
     for (int j = 0; j <= M; ++j)
       hs[r * ps + j] = h[r * (M + 1) + j] * ((j == 0 || j == M) ? 0.5 : 0.25) / (double)M;
   double* phis = nullptr;
@@ -547,6 +548,7 @@ int launch_fstage(cg_plan* p, const double* Win, const double* Gext, bool fused_
   sp.n2 = p->n2;
   sp.n3 = p->n3;
   sp.ncomp = p->C;
+  sp.opb = p->NO == p->C ? 0 : p->C;
   sp.batch = p->B;
   sp.npts = p->npts;
   sp.rho_b = p->rho_b;
@@ -576,7 +578,7 @@ int launch_theta(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
   tp.A = st.tA;
   tp.Bc = st.tBc;
   tp.nfield = p->B * p->C;
-  tp.ncomp = p->C;
+  tp.ncomp = p->NO;  // operator set of field f = f % NO
   tp.npts = p->npts;
   tp.W = st.tW;
   tp.phi_class_a = st.tclass_mode;
@@ -660,7 +662,7 @@ int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
     gp.N = st.N;
     gp.K = st.K;
     gp.nslab = st.nslab;
-    gp.ncomp = p->C;
+    gp.ncomp = p->NO;  // operator set of field f = f % NO
     gp.nbatch = (int)(nfield * st.nslab);
     gp.tiles_m = (st.M + tc.BM - 1) / tc.BM;
     gp.tiles_n = (st.N + tc.BN - 1) / tc.BN;
@@ -755,7 +757,7 @@ int launch_fused_front(cg_plan* p, const double* Win, bool count_step, cudaStrea
   tp.A = st.tA;
   tp.Bc = 1;
   tp.nfield = p->B * p->C;
-  tp.ncomp = p->C;
+  tp.ncomp = p->NO;  // operator set of field f = f % NO
   tp.npts = p->npts;
   tp.phi_class_a = st.tclass_mode;
   tp.nclass = st.tnclass;
@@ -770,6 +772,7 @@ int launch_fused_front(cg_plan* p, const double* Win, bool count_step, cudaStrea
   sp.n2 = p->n2;
   sp.n3 = p->n3;
   sp.ncomp = p->C;
+  sp.opb = p->NO == p->C ? 0 : p->C;
   sp.batch = p->B;
   sp.npts = p->npts;
   sp.rho_b = p->rho_b;
@@ -843,7 +846,7 @@ int setup_fused_front(cg_plan* p) {
 }
 
 int build_stages(cg_plan* p, const cg_desc* d) {
-  const int n1 = p->n1, n2 = p->n2, n3 = p->n3, C = p->C;
+  const int n1 = p->n1, n2 = p->n2, n3 = p->n3, C = p->NO;  // operator sets
   const double* Q = d->Q_theta;
   auto need = [&](const void* ptr, const char* name) -> int {
     if (!ptr) return fail(CG_EINVAL, std::string("missing operand ") + name);
@@ -1036,7 +1039,7 @@ int build_stages(cg_plan* p, const cg_desc* d) {
   return CG_OK;
 }
 
-int bands_upload(cg_plan* p, const double* h, int n, double** out) { return upload(p, h, (size_t)p->C * 3 * n, out); }
+int bands_upload(cg_plan* p, const double* h, int n, double** out) { return upload(p, h, (size_t)p->NO * 3 * n, out); }
 
 }  // namespace
 
@@ -1086,14 +1089,16 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
   p->npts = p->npts_u / p->nl * p->ld;
   p->elems = p->npts * p->B * p->C;
   p->elems_u = p->npts_u * p->B * p->C;
+  if (d->ops_per_run != 0 && d->ops_per_run != 1) return fail(CG_EINVAL, "ops_per_run must be 0 or 1");
+  p->NO = d->ops_per_run ? p->B * p->C : p->C;
 
   int rc = CG_OK;
   auto bail = [&](int code) {
     cg_plan_destroy(p);
     return code;
   };
-  const int C = p->C;
-  if ((rc = upload(p, d->coeff, C, &p->coeff))) return bail(rc);
+  const int C = p->C, NO = p->NO;
+  if ((rc = upload(p, d->coeff, NO, &p->coeff))) return bail(rc);
   if ((rc = upload(p, d->lift, C, &p->lift))) return bail(rc);
   if (d->kin_params && d->nparams > 0) {
     if ((rc = upload(p, d->kin_params, (size_t)p->B * d->nparams, &p->kin_params))) return bail(rc);
@@ -1101,7 +1106,7 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
     return bail(fail(CG_EINVAL, "kinetics parameters missing"));
   }
   if (!d->theta_stencil) return bail(fail(CG_EINVAL, "theta stencil missing"));
-  if ((rc = upload(p, d->theta_stencil, 2 * (size_t)C, &p->th))) return bail(rc);
+  if ((rc = upload(p, d->theta_stencil, 2 * (size_t)NO, &p->th))) return bail(rc);
   int n_rho = 0, n_phi = 0, n_z = 0;
   if (p->geom == CG_DISK) n_rho = p->n1;
   if (p->geom == CG_SPHERE) n_phi = p->n2;
@@ -1116,12 +1121,12 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
   if (n_rho) {
     if (!d->rho_bands || !d->d_rho) return bail(fail(CG_EINVAL, "rho operator missing"));
     if ((rc = bands_upload(p, d->rho_bands, n_rho, &p->rho_b))) return bail(rc);
-    if ((rc = upload(p, d->d_rho, (size_t)C * n_rho, &p->d_rho))) return bail(rc);
+    if ((rc = upload(p, d->d_rho, (size_t)NO * n_rho, &p->d_rho))) return bail(rc);
   }
   if (n_phi) {
     if (!d->phi_bands || !d->d_phi) return bail(fail(CG_EINVAL, "phi operator missing"));
     if ((rc = bands_upload(p, d->phi_bands, n_phi, &p->phi_b))) return bail(rc);
-    if ((rc = upload(p, d->d_phi, (size_t)C * n_phi, &p->d_phi))) return bail(rc);
+    if ((rc = upload(p, d->d_phi, (size_t)NO * n_phi, &p->d_phi))) return bail(rc);
   }
   if (n_z) {
     if (!d->z_bands) return bail(fail(CG_EINVAL, "z operator missing"));
@@ -1250,6 +1255,7 @@ int cg_apply_diffusion(cg_plan* p, const double* W, double* out, void* stream) {
   sp.n2 = p->n2;
   sp.n3 = p->n3;
   sp.ncomp = p->C;
+  sp.opb = p->NO == p->C ? 0 : p->C;
   sp.batch = p->B;
   sp.npts = p->npts;
   sp.rho_b = p->rho_b;
@@ -1278,6 +1284,7 @@ int cg_kinetics(cg_plan* p, const double* W, double* G, void* stream) {
   sp.n2 = p->n2;
   sp.n3 = p->n3;
   sp.ncomp = p->C;
+  sp.opb = p->NO == p->C ? 0 : p->C;
   sp.batch = p->B;
   sp.npts = p->npts;
   sp.lift = p->lift;

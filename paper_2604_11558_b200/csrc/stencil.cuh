@@ -21,6 +21,7 @@ struct StencilParams {
   int geometry;
   int n1, n2, n3;
   int ncomp, batch;
+  int opb;              // operator-set stride per run: 0 (shared) or ncomp (heterogeneous ensemble)
   long long npts;  // points per field (storage)
   // storage layout of the F-build's input W and output F / external G: the
   // contiguous (last) axis has logical extent n_last and row stride ldw / ldf
@@ -167,6 +168,7 @@ struct RowCoef {              // walked-axis tridiagonal row (shared by the CTA,
   double a, b, c, d;          // a_i, b_i (0 at the last row), c_{i-1} (0 at the first), d_rho[i]
 };
 
+// c = operator set index (component, or run * ncomp + component)
 template <int GEOM>
 __device__ __forceinline__ CompCoef comp_coef(const StencilParams& p, int c, int l, int nl) {
   CompCoef k;
@@ -222,7 +224,7 @@ __device__ __forceinline__ double diffusion_rows(const CompCoef& k, const RowCoe
 
 // fill the CTA's walked-axis row coefficients for components [0, nc)
 template <int GEOM>
-__device__ __forceinline__ void row_coefs(RowCoef* rcs, const StencilParams& p, int i0, int nc) {
+__device__ __forceinline__ void row_coefs(RowCoef* rcs, const StencilParams& p, int i0, int nc, int ob) {
   using S = FbuildShape<GEOM>;
   const int n1 = p.n1;
   for (int idx = threadIdx.x; idx < nc * S::RB; idx += blockDim.x) {
@@ -230,11 +232,11 @@ __device__ __forceinline__ void row_coefs(RowCoef* rcs, const StencilParams& p, 
     const int i = min(i0 + r, n1 - 1);
     RowCoef rc{0.0, 0.0, 0.0, 0.0};
     if (GEOM != 1) {
-      const double* bands = p.rho_b + (long long)c * 3 * n1;
+      const double* bands = p.rho_b + (long long)(ob + c) * 3 * n1;
       rc.a = bands[i];
       rc.b = (i < n1 - 1) ? bands[n1 + i] : 0.0;
       rc.c = (i > 0) ? bands[2 * n1 + i - 1] : 0.0;
-      rc.d = p.d_rho[c * n1 + i];
+      rc.d = p.d_rho[(long long)(ob + c) * n1 + i];
     }
     rcs[idx] = rc;
   }
@@ -259,17 +261,18 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
   const long long wbase = (long long)b * p.ncomp * p.npw + (long long)j * (S::D3 ? p.ldw : 0);
   const long long fbase = (long long)b * p.ncomp * p.npf + (long long)j * (S::D3 ? p.ldf : 0);
   const int plane = S::ROWS * nl;
+  const int ob = b * p.opb;  // this run's operator sets
 
   if (KIN == KIN_EXTERNAL) {
     const int nc = p.ncomp < 8 ? p.ncomp : 8;
-    row_coefs<GEOM>(rcs, p, i0, nc);
+    row_coefs<GEOM>(rcs, p, i0, nc, ob);
     for (int c = 0; c < p.ncomp; ++c) {
       const double* X = p.W + wbase + (long long)c * p.npw;
       if (c > 0) __syncthreads();
       stage_rows<GEOM>(fb_smem, X, i0, j, n1, p.n2, nl, rsw, p.ldw);
       __syncthreads();
       if (l < nl) {
-        const CompCoef k = comp_coef<GEOM>(p, c, l, nl);
+        const CompCoef k = comp_coef<GEOM>(p, ob + c, l, nl);
 #pragma unroll
         for (int r = 0; r < S::RB; ++r) {
           const int i = i0 + r;
@@ -284,13 +287,13 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
     }
   } else {
     const bool with_d = p.with_diffusion;
-    if (with_d) row_coefs<GEOM>(rcs, p, i0, 2);
+    if (with_d) row_coefs<GEOM>(rcs, p, i0, 2, ob);
     stage_rows<GEOM>(fb_smem, p.W + wbase, i0, j, n1, p.n2, nl, rsw, p.ldw);
     stage_rows<GEOM>(fb_smem + plane, p.W + wbase + p.npw, i0, j, n1, p.n2, nl, rsw, p.ldw);
     CompCoef k0{}, k1{};  // operator coefficients are only present when diffusing
     if (with_d) {
-      k0 = comp_coef<GEOM>(p, 0, lcl, nl);
-      k1 = comp_coef<GEOM>(p, 1, lcl, nl);
+      k0 = comp_coef<GEOM>(p, ob, lcl, nl);
+      k1 = comp_coef<GEOM>(p, ob + 1, lcl, nl);
     }
     double kin[9];
 #pragma unroll

@@ -57,14 +57,27 @@ def ensemble_plan(template, kin_kind: str, params: np.ndarray, tau: float, theta
     return SplitPlan(geos, batch=params.shape[0], kinetics=kin_kind, kin_params=params, lifts=lifts, theta=theta)
 
 
-def _check_shared(systems):
+def _check_shared(systems) -> bool:
+    """True when every member shares the first member's operators (one
+    operator set per component); False for a heterogeneous ensemble (per-run
+    operator sets: coefficients or domain sizes differ, grids agree).  Names,
+    lifts and the kinetics kind must always agree."""
     ref = systems[0]
+    shared = True
+    shape = [tuple(c.ops.shape) for c in ref.components]
     for s in systems[1:]:
+        if [c.name for c in s.components] != [c.name for c in ref.components]:
+            raise NotImplementedError("ensemble members must have the same components")
+        if [tuple(c.ops.shape) for c in s.components] != shape:
+            raise NotImplementedError("ensemble members must share grid extents")
         for a, b in zip(ref.components, s.components):
-            if a.name != b.name or a.ops is not b.ops and not _same_ops(a.ops, b.ops) or a.lift != b.lift:
-                raise NotImplementedError("ensemble members must share operators, coefficients and lifts")
+            if a.lift != b.lift:
+                raise NotImplementedError("ensemble members must share lifts")
+            if a.ops is not b.ops and not _same_ops(a.ops, b.ops):
+                shared = False
         if engine_kinetics(s).kind != engine_kinetics(ref).kind:
             raise NotImplementedError("ensemble members must share the kinetics kind")
+    return shared
 
 
 def _same_ops(x, y) -> bool:
@@ -147,9 +160,11 @@ class EnsembleResult:
 def run_ensemble(systems, m: int, t_star: float, *, group=None, gather: bool = True,
                  as_torch: bool = False, raise_on_divergence: bool = False,
                  record_every: int | None = None, diagnostics=None) -> EnsembleResult:
-    """Advance every member of ``systems`` (a list of CoupledSystem sharing
-    operators) by m steps of tau = t*/m; shard over the torch.distributed
-    group when one is initialised.
+    """Advance every member of ``systems`` (a list of CoupledSystem on one
+    grid) by m steps of tau = t*/m; shard over the torch.distributed group
+    when one is initialised.  Members sharing their operators run on one
+    operator set per component; members that differ (diffusion coefficients,
+    domain sizes: a parameter sweep) get one prepared set per run.
 
     ``diagnostics`` (a ``models.MeanDiagnostics``, e.g.
     ``mean_diagnostics(systems[0])``) samples every member's integral means on
@@ -185,10 +200,17 @@ def run_ensemble(systems, m: int, t_star: float, *, group=None, gather: bool = T
     names = [c.name for c in systems[0].components]
     ncomp = len(names)
     if mine:
-        _check_shared(mine)
+        shared = _check_shared(mine)
         kin = engine_kinetics(mine[0])
         params = np.stack([engine_kinetics(s).param_vector() for s in mine])
-        plan = ensemble_plan(mine[0], kin.kind, params, tau)
+        if shared:
+            plan = ensemble_plan(mine[0], kin.kind, params, tau)
+        else:
+            # heterogeneous ensemble: one prepared operator set per (run, component)
+            geos = [prepare(c.ops, tau) for s in mine for c in s.components]
+            lifts = [float(getattr(c, "lift", 0.0)) for c in mine[0].components]
+            plan = SplitPlan(geos, batch=len(mine), kinetics=kin.kind, kin_params=params, lifts=lifts,
+                             ops_per_run=True)
         host = np.stack([np.stack([np.asarray(c.initial, dtype=np.float64) for c in s.components]) for s in mine])
         state = torch.from_numpy(np.ascontiguousarray(host)).to("cuda")
         first_bad = torch.full((hi - lo, plan.ncomp), INT32_MAX, dtype=torch.int32, device="cuda")

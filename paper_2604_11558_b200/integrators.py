@@ -224,12 +224,18 @@ class SplitPlan:
     """
 
     def __init__(self, geos, batch: int = 1, kinetics: str = "external",
-                 kin_params=None, lifts=None, theta: str | None = None):
+                 kin_params=None, lifts=None, theta: str | None = None, ops_per_run: bool = False):
+        """``geos``: one GeometryOps per component, shared by the ``batch``
+        runs; with ``ops_per_run`` one per (run, component) in run-major
+        order (a heterogeneous ensemble: runs may differ in coefficients and
+        domain sizes, the grid extents must agree)."""
         import torch  # noqa: F401  (device memory / streams)
 
         geos = list(geos)
         if not geos:
             raise ValueError("need at least one component")
+        if ops_per_run and len(geos) % int(batch) != 0:
+            raise ValueError("ops_per_run needs batch * ncomp operator sets")
         g = _geometry_name(geos[0].geometry)
         shape = tuple(geos[0].shape)
         taus = {float(o.tau) for o in geos}
@@ -243,7 +249,8 @@ class SplitPlan:
         self.geometry = g
         self.shape = shape
         self.batch = int(batch)
-        self.ncomp = len(geos)
+        self.ncomp = len(geos) // self.batch if ops_per_run else len(geos)
+        self.ops_per_run = bool(ops_per_run)
         self.tau = taus.pop()
         C = self.ncomp
         keep = {}
@@ -298,6 +305,7 @@ class SplitPlan:
         # 'fft' applies where n_theta is a power of two, else the plan keeps the GEMM pair
         self.theta = theta
         d.options = _native.CG_OPT_THETA_FFT if theta == "fft" else 0
+        d.ops_per_run = 1 if ops_per_run else 0
         if kin_params is not None:
             kp = _f64(kin_params).reshape(self.batch, -1)
             keep[id(kp)] = kp
