@@ -145,28 +145,66 @@ def _rho_weights(base):
     return base.rho.grid**-2.0
 
 
+_OP_CACHE: dict = {}
+_OP_CACHE_MAX = 64
+
+
+def _op_key(op):
+    parts = [type(op).__name__, getattr(op, "n", None), getattr(op, "h", None),
+             str(getattr(op, "kind", ""))]
+    for attr in ("a", "b", "c", "grid", "diag", "off"):
+        v = getattr(op, attr, None)
+        parts.append(None if v is None else np.asarray(v, dtype=np.float64).tobytes())
+    return tuple(parts)
+
+
+def _cached(op, what, fn):
+    """Coefficient-independent setup of a 1-D operator (eigenpairs, dense
+    copy), shared by every component / run that uses an operator with the
+    same content -- a heterogeneous ensemble prepares one operator set per
+    run, and these products are the same for all of them.  The results are
+    read-only, as the reference treats prepared operands."""
+    key = (what,) + _op_key(op)
+    hit = _OP_CACHE.get(key)
+    if hit is None:
+        hit = fn(op)
+        for arr in (hit if isinstance(hit, tuple) else (hit,)):
+            for v in (vars(arr).values() if hasattr(arr, "__dict__") else (arr,)):
+                if isinstance(v, np.ndarray):
+                    v.flags.writeable = False
+        if len(_OP_CACHE) >= _OP_CACHE_MAX:
+            _OP_CACHE.pop(next(iter(_OP_CACHE)))
+        _OP_CACHE[key] = hit
+    return hit
+
+
 def prepare(base, tau: float) -> GeometryOps:
     """Host setup of every transform and phi1 factor for one component at a
     fixed step (integrators.py:130-173).  Dense A_* copies are kept for API
-    parity; the engine applies the stencils from the bands."""
+    parity; the engine applies the stencils from the bands.  Eigenpairs and
+    dense operator copies are cached by operator content (_cached): only the
+    phi1 factors depend on tau * coeff."""
     if tau < 0:
         raise ValueError("tau must be nonnegative")
     g = _geometry_name(base.geometry)
     s = tau * base.coeff
     kw: dict = {}
     if base.theta is not None:
-        fac = eig_theta(base.theta)
-        kw.update(A_theta=base.theta.toarray(), Q_theta=fac.Q, lam_theta=fac.lambdas)
+        fac = _cached(base.theta, "eig_theta", eig_theta)
+        kw.update(A_theta=_cached(base.theta, "dense", lambda o: o.toarray()), Q_theta=fac.Q,
+                  lam_theta=fac.lambdas)
     if base.rho is not None:
-        kw.update(A_rho=base.rho.toarray(), d_rho=_rho_weights(base),
-                  phi1_rho=phi1_matrix(s, eig_tridiag(base.rho)))
+        kw.update(A_rho=_cached(base.rho, "dense", lambda o: o.toarray()), d_rho=_rho_weights(base),
+                  phi1_rho=phi1_matrix(s, _cached(base.rho, "eig", eig_tridiag)))
     if base.phi is not None:
-        fac = eig_tridiag(base.phi)
-        kw.update(A_phi=base.phi.toarray(), d_phi=np.sin(base.phi.grid) ** -2.0, phi_fac=fac)
+        fac = _cached(base.phi, "eig", eig_tridiag)
+        kw.update(A_phi=_cached(base.phi, "dense", lambda o: o.toarray()),
+                  d_phi=_cached(base.phi, "sin2", lambda o: np.sin(o.grid) ** -2.0), phi_fac=fac)
         if g == "sphere":
             kw["phi1_phi"] = phi1_matrix(s, fac)
     if base.z is not None:
-        kw.update(A_z=base.z.toarray(), phi1_z=phi1_matrix(s, eig_tridiag(base.z)))
+        kw.update(A_z=_cached(base.z, "dense", lambda o: o.toarray()),
+                  phi1_z=phi1_matrix(s, _cached(base.z, "eig", eig_tridiag)))
     if g == "disk":
         kw["phi_mix"] = phi1_outer(s, [kw["d_rho"], kw["lam_theta"]])
     elif g == "sphere":
