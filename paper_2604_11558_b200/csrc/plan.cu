@@ -475,6 +475,8 @@ int add_stage(cg_plan* p, int var, int epi, int M, int N, int K, int nslab, int 
 double* buf_ptr(cg_plan* p, int id, double* out) { return id == BUF_X ? p->X : id == BUF_Y ? p->Y : out; }
 
 bool pow2(int n) { return n >= 4 && (n & (n - 1)) == 0; }
+// theta extents the FFT propagator handles: powers of two, and 100 (M = 5 x 10)
+bool fft_extent(int n) { return pow2(n) || n == 100; }
 
 // row stride of the scaled Phi table: M + 1 rounded up to a multiple of 8
 // doubles that is an odd multiple of 8 (two lines 64 bytes apart per half-warp)
@@ -621,6 +623,13 @@ int launch_theta(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
     if (ax)                                                                                          \
       return launch_pdl(theta_fast_kernel<M1, M2, true>, dim3(nb), dim3(256), FastTheta<M1, M2>::smem, s, tp); \
     return launch_pdl(theta_fast_kernel<M1, M2, false>, dim3(nb), dim3(256), FastTheta<M1, M2>::smem, s, tp); \
+  }
+  // M = 50 (n_theta = 100): 5 threads per line, 20 lines per 100-thread CTA
+  if (st.N == 100 && span % 20 == 0) {
+    using F5 = FastTheta<5, 10, 100>;
+    const unsigned nb = (unsigned)(lines / F5::LPB);
+    if (ax) return launch_pdl(theta_fast_kernel<5, 10, true, 100>, dim3(nb), dim3(100), F5::smem, s, tp);
+    return launch_pdl(theta_fast_kernel<5, 10, false, 100>, dim3(nb), dim3(100), F5::smem, s, tp);
   }
   TRY_FAST(4, 4)
   TRY_FAST(4, 8)
@@ -891,7 +900,7 @@ int build_stages(cg_plan* p, const cg_desc* d) {
     return add_stage(p, VAR_NN, EPI_AXPY, n1, n2 * n3, n1, 1, BUF_X, BUF_OUT, n1,
                      [&](int c, int r, int q) { return P1[((size_t)c * n1 + r) * n1 + q]; });
   }
-  if (p->geom == CG_BALL && fft && pow2(n2)) {
+  if (p->geom == CG_BALL && fft && fft_extent(n2)) {
     if ((rc = need(d->phi1_rho, "phi1_rho")) || (rc = need(d->Phi, "Phi")) ||
         (rc = need(d->Phi_outer, "Phi_outer")) || (rc = need(d->V_phi, "V_phi")) ||
         (rc = need(d->Vinv_phi, "Vinv_phi")))
@@ -1162,6 +1171,11 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
   e2 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,\
                             (int)FastTheta<M1, M2, 64>::smem);                                                \
   if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
+    e1 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, true, 100>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)FastTheta<5, 10, 100>::smem);
+    e2 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, false, 100>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)FastTheta<5, 10, 100>::smem);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
     OPT_IN(4, 4)
     OPT_IN(4, 8)
     OPT_IN(8, 8)

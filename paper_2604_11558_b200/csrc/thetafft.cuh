@@ -14,7 +14,8 @@
 // split/merge twiddles, the real Phi_j scaling, and the inverse, all in
 // shared memory: O(N log N) work instead of 2 N^2 per line, one HBM read and
 // one write per value.  N must be a power of two (radix-4 Stockham stages
-// plus at most one radix-2 stage).
+// plus at most one radix-2 stage) for the Stockham kernel; the register
+// two-phase kernel also takes M = 50 = 5 x 10 (the ball's n_theta = 100).
 //
 // A field is viewed as [A][N][Bc] (A = axes before theta, Bc = axes after);
 // a CTA owns W lines: W consecutive a (Bc == 1, contiguous rows) or W
@@ -344,6 +345,60 @@ __device__ __forceinline__ void dft_reg(double2* a) {
 
 // NT threads per CTA: 256, or 64 for problems with too few lines to give
 // every SM a CTA at 256 (the sphere's 512 theta columns, config 1's disk)
+// Odd-factor DFTs for theta extents that are not powers of two (the ball's
+// n_theta = 100: M = 50 = 5 x 10).  5-point: the real-coefficient pair form
+// (t1 = x1 + x4, t2 = x2 + x3, t3 = x1 - x4, t4 = x2 - x3); 10-point: one
+// radix-2 step over two 5-point DFTs.
+__device__ __forceinline__ double2 mul_mi(double2 v) { return make_double2(v.y, -v.x); }  // -i v
+__device__ __forceinline__ double2 mul_pi(double2 v) { return make_double2(-v.y, v.x); }  // +i v
+
+template <bool INV>
+__device__ __forceinline__ void dft5(double2& x0, double2& x1, double2& x2, double2& x3, double2& x4) {
+  constexpr double c1 = 0.30901699437494745, c2 = -0.8090169943749475;   // cos(2 pi/5), cos(4 pi/5)
+  constexpr double s1 = 0.9510565162951535, s2 = 0.5877852522924731;     // sin(2 pi/5), sin(4 pi/5)
+  const double2 t1 = cadd(x1, x4), t2 = cadd(x2, x3), t3 = csub(x1, x4), t4 = csub(x2, x3);
+  const double2 a1 = make_double2(x0.x + c1 * t1.x + c2 * t2.x, x0.y + c1 * t1.y + c2 * t2.y);
+  const double2 a2 = make_double2(x0.x + c2 * t1.x + c1 * t2.x, x0.y + c2 * t1.y + c1 * t2.y);
+  const double2 b1 = make_double2(s1 * t3.x + s2 * t4.x, s1 * t3.y + s2 * t4.y);
+  const double2 b2 = make_double2(s2 * t3.x - s1 * t4.x, s2 * t3.y - s1 * t4.y);
+  x0 = cadd(x0, cadd(t1, t2));
+  const double2 ib1 = INV ? mul_pi(b1) : mul_mi(b1), ib2 = INV ? mul_pi(b2) : mul_mi(b2);
+  x1 = cadd(a1, ib1);
+  x4 = csub(a1, ib1);
+  x2 = cadd(a2, ib2);
+  x3 = csub(a2, ib2);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft10(double2* a) {
+  double2 e[5] = {a[0], a[2], a[4], a[6], a[8]}, o[5] = {a[1], a[3], a[5], a[7], a[9]};
+  dft5<INV>(e[0], e[1], e[2], e[3], e[4]);
+  dft5<INV>(o[0], o[1], o[2], o[3], o[4]);
+  constexpr double cs[5] = {1.0, 0.8090169943749475, 0.30901699437494745, -0.30901699437494745, -0.8090169943749475};
+  constexpr double sn[5] = {0.0, 0.5877852522924731, 0.9510565162951535, 0.9510565162951535, 0.5877852522924731};
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const double s = INV ? sn[k] : -sn[k];  // w_10^k = cos - i sin (forward)
+    const double2 w = make_double2(o[k].x * cs[k] - o[k].y * s, o[k].x * s + o[k].y * cs[k]);
+    a[k] = cadd(e[k], w);
+    a[k + 5] = csub(e[k], w);
+  }
+}
+
+// DFT of length L in registers, natural order in and out
+template <int L, bool INV>
+__device__ __forceinline__ void dft_any(double2* a) {
+  if constexpr ((L & (L - 1)) == 0) {
+    dft_reg<L, INV>(a);
+  } else if constexpr (L == 5) {
+    dft5<INV>(a[0], a[1], a[2], a[3], a[4]);
+  } else if constexpr (L == 10) {
+    dft10<INV>(a);
+  } else {
+    static_assert(L == 0, "unsupported DFT length");
+  }
+}
+
 template <int M1, int M2, int NT = 256>
 struct FastTheta {
   static constexpr int M = M1 * M2;
@@ -373,7 +428,7 @@ __device__ __forceinline__ T ldt(const T* p) {
 // read consecutive entries instead of a stride of 2 k1, bank-conflict free)
 template <int M1, int M2, bool INV, bool TS = false, bool TA = false>
 __device__ __forceinline__ void phase_a(double2* r, double2* S, int n2, const double2* tw) {
-  dft_reg<M1, INV>(r);
+  dft_any<M1, INV>(r);
 #pragma unroll
   for (int k1 = 1; k1 < M1; ++k1) {
     const double2 w = ldt<TS>(TA ? tw + k1 * M2 + n2 : tw + 2 * n2 * k1);
@@ -404,7 +459,7 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
     const int k1 = lt + q * TPL;
 #pragma unroll
     for (int n2 = 0; n2 < M2; ++n2) keep[q][n2] = S[k1 * (M2 + 1) + n2];
-    dft_reg<M2, false>(keep[q]);
+    dft_any<M2, false>(keep[q]);
   }
   __syncthreads();
 #pragma unroll
@@ -469,7 +524,7 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
     const int k1 = lt + q * TPL;
 #pragma unroll
     for (int n2 = 0; n2 < M2; ++n2) r[n2] = S[k1 * (M2 + 1) + n2];
-    dft_reg<M2, true>(r);
+    dft_any<M2, true>(r);
 #pragma unroll
     for (int k2 = 0; k2 < M2; ++k2) {
       const int k = k1 + M1 * k2;
