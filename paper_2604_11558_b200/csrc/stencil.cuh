@@ -123,7 +123,10 @@ __device__ __forceinline__ double circ3(const double* th, double xm, double x0, 
 template <int GEOM>
 struct FbuildShape {
   static constexpr bool D3 = GEOM >= 2;
-  static constexpr int RB = D3 ? 4 : 8;              // interior rows per CTA
+#ifndef CG_RB3
+#define CG_RB3 4
+#endif
+  static constexpr int RB = D3 ? CG_RB3 : 8;         // interior rows per CTA
   static constexpr int ROWS = D3 ? 3 * RB + 2 : RB + 2;  // staged rows per component
 };
 

@@ -31,30 +31,35 @@ def graph_time(fn, reps=50):
     return e0.elapsed_time(e1) / (5 * reps) * 1e3
 
 
-for k in [int(x) for x in os.environ.get("CONFIGS", "1,2,3").split(",")]:
-    for theta in ("fft", "gemm"):
-        for cfg in (2, 7, 8):
-            os.environ["CURVIGPU_TILE_CFG"] = str(cfg)
-            system = configs.BUILDERS[k]()
-            m, ts = configs.STEPS[k]
-            geos = [prepare(c.ops, ts / m) for c in system.components]
-            plan = SplitPlan(geos, 1, system.kinetics.kind, system.kinetics.param_vector()[None, :], theta=theta)
-            W = torch.from_numpy(np.stack([c.initial for c in system.components])[None].copy()).cuda()
-            out = torch.empty_like(W)
-            bad = torch.full((1, 2), INT32_MAX, dtype=torch.int32, device="cuda")
-            ks = []
-            for st in plan.step_kernels():
-                fl, by = plan.stage_info(st)
-                us = graph_time(lambda: plan.run_stage(st, W, out))
-                ks.append((st, round(us, 2), round(fl / us / 1e6, 2) if fl else None))
-            s = W.clone()
-            plan.run(s, 0, 32, bad)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            plan.run(s, 0, 320, bad)
-            e1.record()
-            e1.synchronize()
-            print(json.dumps({"config": k, "theta": theta, "cfg": cfg, "step_us": round(e0.elapsed_time(e1) / 320 * 1e3, 2),
-                              "kernels_us_tflops": ks}), flush=True)
-            plan.close()
+def main():
+  for k in [int(x) for x in os.environ.get("CONFIGS", "1,2,3").split(",")]:
+      for theta in ("fft", "gemm"):
+          for cfg in (2, 7, 8):
+              os.environ["CURVIGPU_TILE_CFG"] = str(cfg)
+              system = configs.BUILDERS[k]()
+              m, ts = configs.STEPS[k]
+              geos = [prepare(c.ops, ts / m) for c in system.components]
+              plan = SplitPlan(geos, 1, system.kinetics.kind, system.kinetics.param_vector()[None, :], theta=theta)
+              W = torch.from_numpy(np.stack([c.initial for c in system.components])[None].copy()).cuda()
+              out = torch.empty_like(W)
+              bad = torch.full((1, 2), INT32_MAX, dtype=torch.int32, device="cuda")
+              ks = []
+              for st in plan.step_kernels():
+                  fl, by = plan.stage_info(st)
+                  us = graph_time(lambda: plan.run_stage(st, W, out))
+                  ks.append((st, round(us, 2), round(fl / us / 1e6, 2) if fl else None))
+              s = W.clone()
+              plan.run(s, 0, 32, bad)
+              torch.cuda.synchronize()
+              e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+              e0.record()
+              plan.run(s, 0, 320, bad)
+              e1.record()
+              e1.synchronize()
+              print(json.dumps({"config": k, "theta": theta, "cfg": cfg, "step_us": round(e0.elapsed_time(e1) / 320 * 1e3, 2),
+                                "kernels_us_tflops": ks}), flush=True)
+              plan.close()
+
+
+if __name__ == "__main__":
+    main()
