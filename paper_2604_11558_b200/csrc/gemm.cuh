@@ -58,7 +58,7 @@ struct StageBytes {
 
 template <int BM, int BN, int STAGES>
 constexpr int gemm_smem_bytes() {
-  return STAGES * StageBytes<BM, BN>::total + StageBytes<BM, BN>::epi + (2 * STAGES + 4) * 8 + 1024;
+  return STAGES * StageBytes<BM, BN>::total + StageBytes<BM, BN>::epi + (2 * STAGES + 5) * 8 + 1024;
 }
 
 // Row permutation within an 8-row group used by the TN fragments: rows of a
@@ -100,6 +100,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
   uint64_t* epi_empty = epi_full + 1;    // previous tile's store has read etile
   uint64_t* red_full = epi_empty + 1;    // KS > 1, rank 0: the peers' partials are in their etiles
   uint64_t* red_empty = red_full + 1;    // KS > 1, peers: rank 0 has read this CTA's partial
+  uint64_t* epi_ready = red_empty + 1;   // consumers have written the tile's results into etile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KT = (p.K + 15) >> 4;
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
     }
     mbar_init(epi_full, 1);
     mbar_init(epi_empty, 1);
+    mbar_init(epi_ready, 1);
     if constexpr (KS > 1) {
       mbar_init(red_full, (KS - 1) * NCW);
       mbar_init(red_empty, NCW);
@@ -139,10 +141,24 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
   // epilogue of the current one.
   if (warp == NCW) {
     // ---------------- TMA producer ----------------
+    // The producer lane also issues each tile's result store: it waits until
+    // the consumers have written tile t-1 into etile (epi_ready), stores it
+    // while tile t's first k slices are already in flight, and waits for the
+    // store to have read etile before it reuses etile (W tile of the axpy
+    // epilogue) or releases it (epi_empty).  The consumer warps go straight
+    // from one tile's epilogue into the next mainloop.
     if (lane == 0) {
       tma_prefetch_desc(&mapA);
       tma_prefetch_desc(&mapB);
       int it = 0, tc = 0;
+      int pm0 = 0, pn0 = 0, ps = 0, pf = 0;  // previous tile (pending store)
+      auto store_prev = [&](int ptc) {
+        mbar_wait(epi_ready, ptc & 1);
+        if ((pm0 + BM <= p.M) && (pn0 + BN <= p.N)) {  // partial tiles were stored from registers
+          tma_store_4d(&mapO, etile, pn0, pm0, ps, pf);
+          bulk_commit();
+        }
+      };
       for (int tile = KS > 1 ? cid : (int)blockIdx.x; tile < ntiles; tile += KS > 1 ? ncl : (int)gridDim.x, ++tc) {
         int r = tile;
         const int tn = r % p.tiles_n;
@@ -152,7 +168,10 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
         const int f = t / p.nslab, s = t - f * p.nslab;
         const int c = f % p.ncomp;
         const int m0 = tm * BM, n0 = tn * BN;
-        for (int kt = KS > 1 ? kt_begin : 0; kt < (KS > 1 ? kt_end : KT); ++kt, ++it) {
+        const int kb = KS > 1 ? kt_begin : 0, ke = KS > 1 ? kt_end : KT;
+        const int kstore = kb + (ke - kb < STAGES ? ke - kb : STAGES);  // slices issued before the previous store
+        for (int kt = kb; kt < ke; ++kt, ++it) {
+          if (rank == 0 && tc > 0 && kt == kstore) store_prev(tc - 1);
           const int st = it % STAGES;
           if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
           uint8_t* sa = smem + st * STAGE;
@@ -168,12 +187,25 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
             for (int q = 0; q < BN / 16; ++q) tma_load_4d(sb + q * 2048, &mapB, &full[st], n0 + 16 * q, kt * 16, s, f);
           }
         }
-        if (EPI == EPI_AXPY && rank == 0) {
-          // W tile for this tile's epilogue, once the previous tile's store has drained etile
-          if (tc > 0) mbar_wait(epi_empty, (tc - 1) & 1);
-          mbar_arrive_expect_tx(epi_full, EPIB);
-          tma_load_4d(etile, &mapW, epi_full, n0, m0, s, f);
+        if (rank == 0) {
+          if (tc > 0) {
+            if (kstore == ke) store_prev(tc - 1);
+            bulk_wait_read0();      // the previous tile's store has read etile
+            mbar_arrive(epi_empty);
+          }
+          if (EPI == EPI_AXPY) {  // W tile for this tile's epilogue
+            mbar_arrive_expect_tx(epi_full, EPIB);
+            tma_load_4d(etile, &mapW, epi_full, n0, m0, s, f);
+          }
         }
+        pm0 = m0;
+        pn0 = n0;
+        ps = s;
+        pf = f;
+      }
+      if (rank == 0 && tc > 0) {
+        store_prev(tc - 1);
+        bulk_wait0();
       }
     }
     if (KS > 1) {
@@ -402,20 +434,12 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
     }
     fence_proxy_async_smem();
     named_bar(1, NCW * 32);
-    if (threadIdx.x == 0) {
-      if (full_tile) {
-        tma_store_4d(&mapO, etile, n0, m0, s, f);
-        bulk_commit();
-        bulk_wait_read0();
-      }
-      mbar_arrive(epi_empty);
-    }
-    __syncwarp();  // reconverge warp 0 (lane 0 ran the store) before the next tile's MMAs
+    if (threadIdx.x == 0) mbar_arrive(epi_ready);  // the producer lane stores the tile
+    __syncwarp();  // reconverge warp 0 before the next tile's MMAs
     if (EPI == EPI_AXPY) {
       if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(p.first_bad + f, step_now);
     }
   }
-  if (threadIdx.x == 0) bulk_wait0();
   if (KS > 1) {
     __syncwarp();
     cluster_sync_all();

@@ -66,6 +66,40 @@ __global__ void dfma_loop(double* out, int iters, double seed) {
   if (s == 1.2345) out[0] = s;
 }
 
+// Mixed probe: on every SM sub-partition half the warps run DMMA, half DFMA.
+// If both rates add up past ~37 TF the two instruction kinds use separate pipes.
+template <int NACC>
+__global__ void mixed_loop(double* out, int iters, int dfma_iters, double seed) {
+  const int warp = threadIdx.x >> 5;
+  double s = 0;
+  if (((warp >> 2) & 1) == 0) {  // warps 0-3, 8-11: DMMA; every SMSP (warp % 4) gets both kinds
+    double a = seed + threadIdx.x, b = seed * 0.5 + threadIdx.x;
+    double c[NACC][2];
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) { c[i][0] = 0.0; c[i][1] = 0.0; }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < NACC; ++i)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) s += c[i][0] + c[i][1];
+  } else {
+    double x[NACC];
+    double a = seed + threadIdx.x * 1e-9, b = 1.0 - 1e-12;
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) x[i] = i;
+    for (int it = 0; it < dfma_iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < NACC; ++i) x[i] = fma(x[i], b, a);
+    }
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) s += x[i];
+  }
+  if (s == 1.2345) out[0] = s;
+}
+
 int main() {
   double* d; CK(cudaMalloc(&d, 8));
   cudaDeviceProp prop; CK(cudaGetDeviceProperties(&prop, 0));
@@ -109,6 +143,22 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     double flops = 5.0 * blocks * threads * (double)iters * 16 * 2.0;
     printf("DFMA          warps/blk %2d blk/sm 2 : %.2f TFLOP/s\n", warps, flops / ms / 1e9);
+  }
+  // mixed: half the warps DMMA, half DFMA; time each kind alone (the other
+  // half idle) and together
+  for (int ratio : {0, 8, 16, 32}) {
+    int threads = 512, blocks = sms * 2, iters = 20000;
+    int dfi = iters * ratio / 16;  // DFMA iterations (16 FMAs each) per DMMA iteration count
+    mixed_loop<16><<<blocks, threads>>>(d, 10, 10, 1.0);
+    CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0);
+    for (int r = 0; r < 3; ++r) mixed_loop<16><<<blocks, threads>>>(d, iters, dfi, 1.0);
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double fd = 3.0 * blocks * 8 * (double)iters * 16 * 512.0;
+    double ff = 3.0 * blocks * 8 * 32 * (double)dfi * 16 * 2.0;
+    printf("MIXED dfma/dmma iters %2d/16: DMMA %.2f + DFMA %.2f = %.2f TFLOP/s (%.3f ms)\n", ratio, fd / ms / 1e9,
+           ff / ms / 1e9, (fd + ff) / ms / 1e9, ms / 3);
   }
   // sustained DMMA for ~4 s
   {
