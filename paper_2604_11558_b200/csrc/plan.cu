@@ -117,10 +117,11 @@ int make_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
 struct TileCfg {
   int BM, BN;
 };
-constexpr int kNumCfg = 9;
+constexpr int kNumCfg = 12;
 // 7, 8: the 64x64 configuration split-K over clusters of 2 / 4 CTAs
+// 9, 10: 64x64 tiles on 8 consumer warps (32x16 / 16x32 warp tiles); 11: 10 split-K over 2-CTA clusters
 constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {64, 128}, {128, 128}, {64, 64},
-                                    {64, 64}, {64, 64}};
+                                    {64, 64}, {64, 64}, {64, 64}, {64, 64}, {64, 64}};
 
 // BM, BN, warp tile, stages; 32x32 warp tiles keep the accumulators +
 // fragments under ~160 registers without spills.
@@ -132,6 +133,8 @@ constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {
 #define CFG4 64, 128, 32, 32, 4, 2
 #define CFG5 128, 128, 32, 32, 3, 1
 #define CFG6 64, 64, 32, 32, 6, 3
+#define CFG9 64, 64, 32, 16, 4, 2
+#define CFG10 64, 64, 16, 32, 4, 2
 
 // configure_only: set the dynamic shared memory opt-in (done at plan
 // creation, never inside a stream capture).  KS > 1 launches clusters of KS
@@ -225,6 +228,9 @@ int launch_gemm_cfg(int cfg, const Maps& m, const GemmParams& p, cudaStream_t st
     case 5: return launch_gemm_t<VAR, CFG5, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
     case 7: return launch_gemm_t<VAR, CFG2, EPI, 2>(m.a, m.b, m.w, m.o, p, stream, conf);
     case 8: return launch_gemm_t<VAR, CFG2, EPI, 4>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case 9: return launch_gemm_t<VAR, CFG9, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case 10: return launch_gemm_t<VAR, CFG10, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case 11: return launch_gemm_t<VAR, CFG10, EPI, 2>(m.a, m.b, m.w, m.o, p, stream, conf);
     default: return launch_gemm_t<VAR, CFG6, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
   }
 }
@@ -419,7 +425,10 @@ int pick_cfg(int var, long long nbatch, int M, int N, int K, int stage_index) {
   // Measured on B200 with the TMA epilogue (tools/sweep_tiles.py,
   // profiles/r01_tile_sweep_tmaepi.txt): 64x64 tiles, 4-stage ring, 2 CTAs/SM
   // is the best or within 2% of the best for every stage of every BASELINE
-  // config (larger epilogue tiles cost occupancy).  Stages with too few tiles
+  // config (larger epilogue tiles cost occupancy).  Splitting the 64x64 tile
+  // over 8 consumer warps (16x32 warp tiles, cfg 10) instead of 4 hides more
+  // DMMA/fragment latency: config 5 rho stage 283 -> 277 us, ball stages
+  // -7 to -10 %, config 1 5.7 -> 5.1 us (profiles/r01_warp8_sweep.txt).  Stages with too few tiles
   // to fill the chip split each tile's k range over a cluster of 2 CTAs when
   // every rank keeps >= 4 k slices (tools/small_gemm_sweep.py,
   // profiles/r01_splitk_sweep.jsonl: the sphere's 64-tile stages 13.7 -> 10.9
@@ -437,9 +446,9 @@ int pick_cfg(int var, long long nbatch, int M, int N, int K, int stage_index) {
   const long long tiles = nbatch * ((M + 63) / 64) * ((N + 63) / 64);
   const int KT = (K + 15) / 16;
   if (!getenv("CURVIGPU_NO_SPLITK")) {
-    if (tiles * 2 <= 2LL * sms && KT >= 8) return 7;
+    if (tiles * 2 <= 2LL * sms && KT >= 8) return 11;
   }
-  return 2;
+  return 10;
 }
 
 // Build one GEMM stage: operator L (n x n) via `get`, shapes, epilogue.
@@ -848,6 +857,7 @@ int setup_fused_front(cg_plan* p) {
   const long long items256 = (long long)p->B * (p->n1 / (lpb / 2));
   if (items256 < sms && p->n1 % (lpb / 8) == 0 && (lpb / 8) % 2 == 0 && !getenv("CURVIGPU_NO_SMALL_CTA"))
     p->fused_nt = 64;
+  if (getenv("CURVIGPU_FRONT_NT64") && p->n1 % (lpb / 8) == 0 && (lpb / 8) % 2 == 0) p->fused_nt = 64;  // measurement knob
   int rc = launch_fused_front(p, nullptr, false, nullptr, true);
   if (rc) return rc;
   p->fused_front = true;

@@ -330,13 +330,16 @@ def test_odd_contiguous_axis_runs_match_oracle(k, dims):
         assert rel_inf(res.fields[c.name], ref[c.name]) <= STEP1_TOL, c.name
 
 
-@pytest.mark.parametrize("cfg", ["7", "8"])
+@pytest.mark.parametrize("cfg", ["2", "7", "8", "9", "11"])
 @pytest.mark.parametrize("k,dims", [(2, (24, 16)), (4, (10, 12, 10)), (1, (16, 32)), (3, (8, 16, 16))])
 def test_cluster_split_k_gemm_matches_oracle_and_reruns(monkeypatch, cfg, k, dims):
-    """Every GEMM stage forced onto the split-K cluster kernel (cfg 7: 2-CTA,
-    cfg 8: 4-CTA clusters, partials reduced over DSMEM in rank order), incl.
-    ranks with no k slice at all (K = 16 with 2 or 4 ranks): same results as
-    the oracle within the single-op tolerance and bitwise-identical reruns."""
+    """Every GEMM stage forced onto one tile configuration: the split-K cluster
+    kernels (cfg 7: 2-CTA, cfg 8: 4-CTA clusters, cfg 11: 2-CTA clusters of
+    8-warp CTAs, partials reduced over DSMEM in rank order), incl.
+    ranks with no k slice at all (K = 16 with 2 or 4 ranks), and the
+    non-default single-CTA tiles (cfg 2: 4 warps of 32x32, cfg 9: 8 warps of
+    32x16): same results as the oracle within the single-op tolerance and
+    bitwise-identical reruns."""
     monkeypatch.setenv("CURVIGPU_TILE_CFG", cfg)
     sysm = pcfg.BUILDERS[k](dims)
     m, t = 6, {1: 6e-3, 2: 6e-3, 3: 3.0, 4: 6e-2}[k]
