@@ -117,11 +117,13 @@ int make_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
 struct TileCfg {
   int BM, BN;
 };
-constexpr int kNumCfg = 12;
+constexpr int kNumCfg = 14;
 // 7, 8: the 64x64 configuration split-K over clusters of 2 / 4 CTAs
 // 9, 10: 64x64 tiles on 8 consumer warps (32x16 / 16x32 warp tiles); 11: 10 split-K over 2-CTA clusters
+// 12: 32x32 tiles on 4 warps of 16x16 (stages with very few 64x64 tiles); 13: 12 split-K over 2-CTA clusters
 constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {64, 128}, {128, 128}, {64, 64},
-                                    {64, 64}, {64, 64}, {64, 64}, {64, 64}, {64, 64}};
+                                    {64, 64}, {64, 64}, {64, 64}, {64, 64}, {64, 64},
+                                    {32, 32}, {32, 32}};
 
 // BM, BN, warp tile, stages; 32x32 warp tiles keep the accumulators +
 // fragments under ~160 registers without spills.
@@ -135,6 +137,7 @@ constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {
 #define CFG6 64, 64, 32, 32, 6, 3
 #define CFG9 64, 64, 32, 16, 4, 2
 #define CFG10 64, 64, 16, 32, 4, 2
+#define CFG12 32, 32, 16, 16, 4, 4
 
 // configure_only: set the dynamic shared memory opt-in (done at plan
 // creation, never inside a stream capture).  KS > 1 launches clusters of KS
@@ -231,6 +234,8 @@ int launch_gemm_cfg(int cfg, const Maps& m, const GemmParams& p, cudaStream_t st
     case 9: return launch_gemm_t<VAR, CFG9, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
     case 10: return launch_gemm_t<VAR, CFG10, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
     case 11: return launch_gemm_t<VAR, CFG10, EPI, 2>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case 12: return launch_gemm_t<VAR, CFG12, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case 13: return launch_gemm_t<VAR, CFG12, EPI, 2>(m.a, m.b, m.w, m.o, p, stream, conf);
     default: return launch_gemm_t<VAR, CFG6, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
   }
 }
@@ -428,13 +433,14 @@ int pick_cfg(int var, long long nbatch, int M, int N, int K, int stage_index) {
   // config (larger epilogue tiles cost occupancy).  Splitting the 64x64 tile
   // over 8 consumer warps (16x32 warp tiles, cfg 10) instead of 4 hides more
   // DMMA/fragment latency: config 5 rho stage 283 -> 277 us, ball stages
-  // -7 to -10 %, config 1 5.7 -> 5.1 us (profiles/r01_warp8_sweep.txt).  Stages with too few tiles
-  // to fill the chip split each tile's k range over a cluster of 2 CTAs when
-  // every rank keeps >= 4 k slices (tools/small_gemm_sweep.py,
+  // -7 to -10 %, config 1 5.7 -> 5.1 us (profiles/r01_warp8_sweep.txt).
+  // Split-K (each tile's k range over a cluster of 2 CTAs) was the earlier
+  // answer to stages with too few tiles (tools/small_gemm_sweep.py,
   // profiles/r01_splitk_sweep.jsonl: the sphere's 64-tile stages 13.7 -> 10.9
   // us; 4-CTA clusters and splits of short k ranges lose to the DSMEM
-  // reduction and cluster handshakes; cfg 8 = 4-CTA clusters stays selectable
-  // through CURVIGPU_TILE_CFG for measurement).
+  // reduction and cluster handshakes; the split-K configurations 7, 8, 11, 13
+  // stay selectable through CURVIGPU_TILE_CFG for measurement and are tested,
+  // but the 32x32 tiles below now beat them).
   (void)var;
   static int sms = 0;
   if (!sms) {
@@ -443,12 +449,15 @@ int pick_cfg(int var, long long nbatch, int M, int N, int K, int stage_index) {
                                                   cudaSuccess)
       sms = 148;
   }
+  // Stages with up to 8 x SMs 64x64 tiles (every stage of configs 1-4) run
+  // 32x32 tiles at 4 CTAs/SM instead: 4x the CTAs to spread the work (config
+  // 1 rho stage 4.98 -> 2.84 us, sphere stage 0 10.5 -> 7.05 us, faster than
+  // the split-K clusters, 10.2 us), and no loss where the 64x64 grid already
+  // has 2 waves (cylinder, ball: equal or 2-6 % faster).  Large stages keep
+  // 64x64 (config 5: 277 vs 309 us) (profiles/r01_warp8_sweep.txt).
+  (void)K;
   const long long tiles = nbatch * ((M + 63) / 64) * ((N + 63) / 64);
-  const int KT = (K + 15) / 16;
-  if (!getenv("CURVIGPU_NO_SPLITK")) {
-    if (tiles * 2 <= 2LL * sms && KT >= 8) return 11;
-  }
-  return 10;
+  return tiles <= 8LL * sms ? 12 : 10;
 }
 
 // Build one GEMM stage: operator L (n x n) via `get`, shapes, epilogue.

@@ -330,7 +330,7 @@ def test_odd_contiguous_axis_runs_match_oracle(k, dims):
         assert rel_inf(res.fields[c.name], ref[c.name]) <= STEP1_TOL, c.name
 
 
-@pytest.mark.parametrize("cfg", ["2", "7", "8", "9", "11"])
+@pytest.mark.parametrize("cfg", ["2", "7", "8", "9", "11", "12", "13"])
 @pytest.mark.parametrize("k,dims", [(2, (24, 16)), (4, (10, 12, 10)), (1, (16, 32)), (3, (8, 16, 16))])
 def test_cluster_split_k_gemm_matches_oracle_and_reruns(monkeypatch, cfg, k, dims):
     """Every GEMM stage forced onto one tile configuration: the split-K cluster
