@@ -469,6 +469,14 @@ def _plan_for(ops) -> SplitPlan:
     return plan
 
 
+def _check_shape(x, shape):
+    """The reference's shape check (integrators.py:178-179), done before any
+    device work so a bad call fails the same way with or without a GPU."""
+    got = tuple(x.shape) if hasattr(x, "shape") else np.shape(x)
+    if tuple(got) != tuple(shape):
+        raise ValueError(f"field shape {tuple(got)} does not match {tuple(shape)}")
+
+
 def _to_device(x, shape):
     import torch
 
@@ -493,6 +501,7 @@ def apply_diffusion(ops: GeometryOps, W):
     """coeff * M W on the GPU (integrators.py:176-199)."""
     import torch
 
+    _check_shape(W, ops.shape)
     plan = _plan_for(ops)
     Wd, is_t = _to_device(W, ops.shape)
     out = torch.empty_like(Wd)
@@ -504,6 +513,8 @@ def step_split(ops: GeometryOps, W, G):
     """One split exponential Euler step on the GPU (integrators.py:247-249)."""
     import torch
 
+    _check_shape(W, ops.shape)
+    _check_shape(G, ops.shape)
     plan = _plan_for(ops)
     Wd, is_t = _to_device(W, ops.shape)
     Gd, _ = _to_device(G, ops.shape)
