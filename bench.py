@@ -407,7 +407,9 @@ def engine_arm(args):
     rows = kernel_roofline(ens.plan, init_dev)
     dom = max((r for r in rows), key=lambda r: r["share_of_step"])
     gemm_flops = sum(ens.plan.stage_info(s)[0] for s in range(ens.plan.stage_count()))
-    launches_per_step = chunk * (1 + ens.plan.stage_count()) + 1
+    # kernels one time step launches (fused front + GEMM in fft mode; launch list:
+    # profiles/r01_v10_launches_summary.txt) x time steps, + the step-counter reset per cg_run
+    launches_per_step = chunk * len(ens.plan.step_kernels()) + 1
     line = {
         "metric": METRIC,
         "value": value,
