@@ -21,6 +21,12 @@
 
 namespace cg {
 
+#ifdef CURVIGPU_NO_REGSPLIT
+constexpr bool kNoRegSplit = true;   // A/B build: split/merge through shared memory
+#else
+constexpr bool kNoRegSplit = false;
+#endif
+
 template <int M1, int M2, int NBUF = 2, int NT = 256>
 struct FusedDisk {
   using F = FastTheta<M1, M2, NT>;
@@ -197,7 +203,7 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
 #pragma unroll
     for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, false, true, true>(keepa[q], S, lt + q * TPL, twa_s);
     const long long obase = (long long)f * fsz + (long long)row * N;
-    theta_tail<M1, M2, false, true>(tp, S, lt, phs + (size_t)ln * PS, tw_s, f, obase, 1, 1, twa_s);
+    theta_tail<M1, M2, false, true, !kNoRegSplit, 1>(tp, S, lt, phs + (size_t)ln * PS, tw_s, f, obase, 1, 1, twa_s);
     // release buffer k: generic-proxy accesses before the async-proxy refill
     fence_proxy_async_smem();
     __syncthreads();

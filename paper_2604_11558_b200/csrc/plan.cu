@@ -628,24 +628,33 @@ int launch_theta(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const bool small_cta = !getenv("CURVIGPU_NO_SMALL_CTA");
-#define TRY_FAST(M1, M2)                                                                             \
-  if (st.N / 2 == (M1) * (M2) && span % FastTheta<M1, M2>::LPB == 0) {                               \
+#define TRY_FAST_R(M1, M2, R)                                                                        \
+  {                                                                                                  \
     using F64 = FastTheta<M1, M2, 64>;                                                               \
     if (small_cta && lines / FastTheta<M1, M2>::LPB < sms && span % F64::LPB == 0) {                  \
       const unsigned nb = (unsigned)(lines / F64::LPB);                                              \
       if (ax)                                                                                        \
-        return launch_pdl(theta_fast_kernel<M1, M2, true, 64>, dim3(nb), dim3(64), F64::smem, s, tp);  \
-      return launch_pdl(theta_fast_kernel<M1, M2, false, 64>, dim3(nb), dim3(64), F64::smem, s, tp);   \
+        return launch_pdl(theta_fast_kernel<M1, M2, true, 64, R>, dim3(nb), dim3(64), F64::smem, s, tp);  \
+      return launch_pdl(theta_fast_kernel<M1, M2, false, 64, R>, dim3(nb), dim3(64), F64::smem, s, tp);   \
     }                                                                                                \
     const unsigned nb = (unsigned)(lines / FastTheta<M1, M2>::LPB);                                  \
     if (ax)                                                                                          \
-      return launch_pdl(theta_fast_kernel<M1, M2, true>, dim3(nb), dim3(256), FastTheta<M1, M2>::smem, s, tp); \
-    return launch_pdl(theta_fast_kernel<M1, M2, false>, dim3(nb), dim3(256), FastTheta<M1, M2>::smem, s, tp); \
+      return launch_pdl(theta_fast_kernel<M1, M2, true, 256, R>, dim3(nb), dim3(256), FastTheta<M1, M2>::smem, s, tp); \
+    return launch_pdl(theta_fast_kernel<M1, M2, false, 256, R>, dim3(nb), dim3(256), FastTheta<M1, M2>::smem, s, tp); \
+  }
+#define TRY_FAST(M1, M2)                                                                             \
+  if (st.N / 2 == (M1) * (M2) && span % FastTheta<M1, M2>::LPB == 0) {                               \
+    if (tp.Bc == 1) TRY_FAST_R(M1, M2, true)                                                         \
+    TRY_FAST_R(M1, M2, false)                                                                        \
   }
   // M = 50 (n_theta = 100): 5 threads per line, 20 lines per 100-thread CTA
   if (st.N == 100 && span % 20 == 0) {
     using F5 = FastTheta<5, 10, 100>;
     const unsigned nb = (unsigned)(lines / F5::LPB);
+    if (tp.Bc == 1) {
+      if (ax) return launch_pdl(theta_fast_kernel<5, 10, true, 100, true>, dim3(nb), dim3(100), F5::smem, s, tp);
+      return launch_pdl(theta_fast_kernel<5, 10, false, 100, true>, dim3(nb), dim3(100), F5::smem, s, tp);
+    }
     if (ax) return launch_pdl(theta_fast_kernel<5, 10, true, 100>, dim3(nb), dim3(100), F5::smem, s, tp);
     return launch_pdl(theta_fast_kernel<5, 10, false, 100>, dim3(nb), dim3(100), F5::smem, s, tp);
   }
@@ -655,6 +664,7 @@ int launch_theta(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
   TRY_FAST(8, 16)
   TRY_FAST(16, 16)
 #undef TRY_FAST
+#undef TRY_FAST_R
   const unsigned blocks = (unsigned)(lines / tp.W);
   const size_t smem = theta_smem_bytes(st.N, st.tW);
   if (st.epi == EPI_AXPY) return launch_pdl(theta_prop_kernel<true>, dim3(blocks), dim3(256), smem, s, tp);
@@ -1179,20 +1189,26 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
     cudaError_t e2 = cudaFuncSetAttribute(theta_prop_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           100 * 1024);
     if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
-#define OPT_IN(M1, M2)                                                                                        \
-  e1 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+#define OPT_IN_R(M1, M2, R)                                                                                   \
+  e1 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, true, 256, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,\
                             (int)FastTheta<M1, M2>::smem);                                                    \
-  e2 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+  e2 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, false, 256, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,\
                             (int)FastTheta<M1, M2>::smem);                                                    \
   if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));  \
-  e1 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+  e1 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, true, 64, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                             (int)FastTheta<M1, M2, 64>::smem);                                                \
-  e2 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,\
+  e2 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, false, 64, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,\
                             (int)FastTheta<M1, M2, 64>::smem);                                                \
   if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
+#define OPT_IN(M1, M2) OPT_IN_R(M1, M2, false) OPT_IN_R(M1, M2, true)
     e1 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, true, 100>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)FastTheta<5, 10, 100>::smem);
     e2 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, false, 100>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)FastTheta<5, 10, 100>::smem);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
+    e1 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, true, 100, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)FastTheta<5, 10, 100>::smem);
+    e2 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, false, 100, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)FastTheta<5, 10, 100>::smem);
     if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
     OPT_IN(4, 4)
@@ -1201,6 +1217,7 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
     OPT_IN(8, 16)
     OPT_IN(16, 16)
 #undef OPT_IN
+#undef OPT_IN_R
   }
   const size_t bytes = (size_t)p->elems * sizeof(double);
   if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&p->X)))) return bail(rc);

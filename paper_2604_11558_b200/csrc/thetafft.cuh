@@ -443,7 +443,41 @@ __device__ __forceinline__ void phase_a(double2* r, double2* S, int n2, const do
 // split, Phi, merge, inverse FFT, scaled store (+ W + tau*y and the guard).
 // ph = this line's Phi_j row (M + 1 values), tw = the N twiddles; both in
 // global memory, or in shared memory when TS.
-template <int M1, int M2, bool AXPY, bool TS = false>
+// Real split, Phi scaling and merge of one (j, M - j) pair: the arithmetic
+// of the textbook split/merge with every 1/2 and the inverse 1/M folded into
+// the pre-scaled Phi row; returns Z'_j in zj_out and Z'_{M-j} in zm_out.
+__device__ __forceinline__ void split_pair(double2 zj, double2 zm, double2 wj, double pj, double pm, double2& zj_out,
+                                           double2& zm_out) {
+  const double2 e = make_double2(zj.x + zm.x, zj.y - zm.y);    // 2 E_j
+  const double2 o = make_double2(zj.y + zm.y, zm.x - zj.x);    // 2 O_j
+  const double2 wo = cmul(wj, o);
+  const double2 xj = make_double2((e.x + wo.x) * pj, (e.y + wo.y) * pj);
+  const double2 xmj = make_double2((e.x - wo.x) * pm, (wo.y - e.y) * pm);
+  const double2 s1 = make_double2(xj.x + xmj.x, xj.y - xmj.y);
+  const double2 d1 = make_double2(xj.x - xmj.x, xj.y + xmj.y);
+  const double2 wd = cmul(cconj(wj), d1);
+  zj_out = make_double2(s1.x - wd.y, s1.y + wd.x);
+  zm_out = make_double2(s1.x + wd.y, wd.x - s1.y);
+}
+
+__device__ __forceinline__ double2 shfl_d2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+// RS (register split): when a line's TPL = M1 threads are consecutive lanes of
+// one warp, forward phase B leaves thread lt holding Z[lt + M1 k2] (k2 < M2),
+// which are exactly the inputs of its inverse phase-A columns n2 = lt + q M1.
+// The split/merge partner of index j = lt + M1 k2 is M - j = (M1 - lt) +
+// M1 (M2 - 1 - k2), held by lane M1 - lt (lt = 0 pairs with itself: k2 <->
+// M2 - k2).  Each thread computes the pairs of its lower half k2 < M2/2 (both
+// outputs) from its partner's upper half received by shuffle, and sends the
+// partner's outputs back: the phase-B store, the split's shared-memory round
+// trip, the inverse phase-A load and two barriers disappear.  Same pairs,
+// same formulas, so the results equal the shared-memory path bit for bit.
+// BCM: 1 = lines are contiguous rows (Bc == 1), 2 = lines are columns
+// (Bc > 1), 0 = decided at run time.  A compile-time layout keeps the layout
+// branch out of the store loop, so its W loads are batched ahead of the stores.
+template <int M1, int M2, bool AXPY, bool TS = false, bool RS = false, int BCM = 0>
 __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int lt, const double* ph,
                                            const double2* tw, int f, long long base, long long es, int Bc,
                                            const double2* twa = nullptr) {
@@ -452,6 +486,67 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
   constexpr int RMAX = M1 > M2 ? M1 : M2;
   double2 r[RMAX];
   __syncthreads();
+  if constexpr (RS) {
+    static_assert(TPL == M1 && (TPL & (TPL - 1)) == 0 && TPL <= 32 && M2 % 2 == 0, "register split layout");
+    constexpr int H = M2 / 2;
+    // ---------------- forward phase B: row k1 = lt -> keep[k2] = Z[lt + M1 k2]
+    double2 keep[M2];
+#pragma unroll
+    for (int n2 = 0; n2 < M2; ++n2) keep[n2] = S[lt * (M2 + 1) + n2];
+    dft_any<M2, false>(keep);
+    // ---------------- split / Phi / merge in registers
+    const int lane = threadIdx.x & 31;
+    const int src = (lane & ~(TPL - 1)) | ((TPL - lt) & (TPL - 1));
+    const bool z0 = lt == 0;
+    double2 out_hi[H];  // outputs for the partner's slots M2 - 1 - h (lt = 0: own slots M2 - h)
+    double2 selfm{};    // lt = 0: Z'_{M/2}
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const double2 zin = shfl_d2(keep[M2 - 1 - h], src);   // partner's Z[M - j]
+      const double2 zm = z0 ? keep[(M2 - h) & (M2 - 1)] : zin;
+      const int j = lt + M1 * h;
+      const int jm = z0 ? ((M - M1 * h) & (M - 1)) : M - j;
+      const double2 wj = ldt<TS>(tw + j);
+      const double pj = ldt<TS>(ph + j), pm = ldt<TS>(ph + (h == 0 && z0 ? M : jm));
+      double2 oj, om;
+      split_pair(keep[h], zm, wj, pj, pm, oj, om);
+      if (h == 0 && z0) {  // j = 0: DC and Nyquist packed in Z_0
+        const double2 zz = keep[0];
+        const double x0 = (zz.x + zz.y) * pj;
+        const double xm = (zz.x - zz.y) * pm;
+        oj = make_double2(x0 + xm, x0 - xm);
+      }
+      if (h == 0) {
+        // lt = 0 also owns the self-paired j = M/2 (k2 = M2/2)
+        const double2 zh = keep[H];
+        const double ph2 = ldt<TS>(ph + M / 2);
+        double2 oh, unused;
+        split_pair(zh, zh, ldt<TS>(tw + M / 2), ph2, ph2, oh, unused);
+        selfm = oh;
+      }
+      keep[h] = oj;
+      out_hi[h] = om;
+    }
+    // partner's outputs for this thread's upper half
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const double2 back = shfl_d2(out_hi[h], src);
+      // slot M2 - 1 - h: from the partner, or (lt = 0) own pair h + 1 / the M/2 self pair
+      keep[M2 - 1 - h] = z0 ? (h + 1 < H ? out_hi[h + 1] : selfm) : back;
+    }
+    __syncthreads();  // every thread has read its S row (phase B) before phase A overwrites S
+    // ---------------- inverse phase A from registers: column n2 = lt + q M1 holds k2 = q + (M2/M1) n1
+#pragma unroll
+    for (int q = 0; q < M2 / TPL; ++q) {
+      double2 col[M1];
+#pragma unroll
+      for (int n1 = 0; n1 < M1; ++n1) col[n1] = keep[q + (M2 / M1) * n1];
+      if (TS)
+        phase_a<M1, M2, true, true, true>(col, S, lt + q * TPL, twa);
+      else
+        phase_a<M1, M2, true>(col, S, lt + q * TPL, tw);
+    }
+  } else {
   // ---------------- forward phase B: rows k1 = lt, lt + TPL, ...
   double2 keep[M1 / TPL][M2];
 #pragma unroll
@@ -516,12 +611,31 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
     else
       phase_a<M1, M2, true>(keepa[q], S, lt + q * TPL, tw);
   }
+  }  // RS
   __syncthreads();
   // ---------------- inverse phase B + store (y_2k = Re z'_k / M, y_2k+1 = Im z'_k / M)
+  // With a compile-time layout (BCM != 0) the axpy epilogue's W values are
+  // loaded before the row's shared-memory loads and inverse DFT, so their L2
+  // latency hides behind that arithmetic (the small-grid kernels are latency-bound).
   bool bad = false;
+  const bool rows = BCM == 1 || (BCM == 0 && Bc == 1);
+  constexpr bool PRE = AXPY && BCM != 0;
 #pragma unroll
   for (int q = 0; q < M1 / TPL; ++q) {
     const int k1 = lt + q * TPL;
+    double2 wpre[PRE ? M2 : 1];
+    if constexpr (PRE) {
+#pragma unroll
+      for (int k2 = 0; k2 < M2; ++k2) {
+        const int k = k1 + M1 * k2;
+        if (rows) {
+          wpre[k2] = __ldg(reinterpret_cast<const double2*>(p.Wprev + base + 2LL * k));
+        } else {
+          const long long o0 = base + (2LL * k) * es;
+          wpre[k2] = make_double2(__ldg(p.Wprev + o0), __ldg(p.Wprev + o0 + es));
+        }
+      }
+    }
 #pragma unroll
     for (int n2 = 0; n2 < M2; ++n2) r[n2] = S[k1 * (M2 + 1) + n2];
     dft_any<M2, true>(r);
@@ -529,10 +643,10 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
     for (int k2 = 0; k2 < M2; ++k2) {
       const int k = k1 + M1 * k2;
       double y0 = r[k2].x, y1 = r[k2].y;  // 1/M is folded into phis
-      if (Bc == 1) {
+      if (rows) {
         const long long o = base + 2LL * k;
         if (AXPY) {
-          const double2 wv = __ldg(reinterpret_cast<const double2*>(p.Wprev + o));
+          const double2 wv = PRE ? wpre[PRE ? k2 : 0] : __ldg(reinterpret_cast<const double2*>(p.Wprev + o));
           y0 = __dadd_rn(wv.x, __dmul_rn(p.tau, y0));
           y1 = __dadd_rn(wv.y, __dmul_rn(p.tau, y1));
           bad |= !(fabs(y0) <= p.limit) || !(fabs(y1) <= p.limit);
@@ -541,8 +655,10 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
       } else {
         const long long o0 = base + (2LL * k) * es, o1 = o0 + es;
         if (AXPY) {
-          y0 = __dadd_rn(__ldg(p.Wprev + o0), __dmul_rn(p.tau, y0));
-          y1 = __dadd_rn(__ldg(p.Wprev + o1), __dmul_rn(p.tau, y1));
+          const double w0 = PRE ? wpre[PRE ? k2 : 0].x : __ldg(p.Wprev + o0);
+          const double w1 = PRE ? wpre[PRE ? k2 : 0].y : __ldg(p.Wprev + o1);
+          y0 = __dadd_rn(w0, __dmul_rn(p.tau, y0));
+          y1 = __dadd_rn(w1, __dmul_rn(p.tau, y1));
           bad |= !(fabs(y0) <= p.limit) || !(fabs(y1) <= p.limit);
         }
         p.Y[o0] = y0;
@@ -555,17 +671,23 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
   }
 }
 
-template <int M1, int M2, bool AXPY, int NT = 256>
+// ROWS: lines are contiguous rows (Bc == 1), a compile-time split so the
+// column kernels (Bc > 1) keep their own register allocation
+template <int M1, int M2, bool AXPY, int NT = 256, bool ROWS = false>
 __global__ void __launch_bounds__(NT) theta_fast_kernel(const ThetaParams p) {
   pdl_wait();
   using F = FastTheta<M1, M2, NT>;
   constexpr int M = F::M, TPL = F::TPL, LPB = F::LPB;
   extern __shared__ double2 tf_smem[];
   const int N = 2 * M;
-  const int Bc = p.Bc;
+  // the dispatcher picks ROWS = (Bc == 1); the layout is compile-time for row
+  // kernels and axpy column kernels (measured faster), run-time otherwise
+  constexpr int MODE = ROWS ? 1 : (AXPY ? 2 : 0);
+  const int Bc = ROWS ? 1 : p.Bc;
+  const bool rows = MODE == 1 || (MODE == 0 && Bc == 1);
   const int tid = threadIdx.x;
   int ln, lt;  // line within CTA, thread within line
-  if (Bc == 1) {
+  if (rows) {
     ln = tid / TPL;
     lt = tid - ln * TPL;
   } else {
@@ -575,7 +697,7 @@ __global__ void __launch_bounds__(NT) theta_fast_kernel(const ThetaParams p) {
   // CTA -> (field, a0, bc0) with W = LPB lines
   const int blk = blockIdx.x;
   int f, a0, bc0;
-  if (Bc == 1) {
+  if (rows) {
     const int per = p.A / LPB;
     f = blk / per;
     a0 = (blk - f * per) * LPB;
@@ -588,7 +710,7 @@ __global__ void __launch_bounds__(NT) theta_fast_kernel(const ThetaParams p) {
     a0 = pa - f * p.A;
   }
   const int c = f % p.ncomp;
-  const int la = (Bc == 1) ? a0 + ln : a0, lbc = (Bc == 1) ? 0 : bc0 + ln;
+  const int la = rows ? a0 + ln : a0, lbc = rows ? 0 : bc0 + ln;
   const long long lstride = (long long)N * Bc;
   const long long base = (long long)f * p.npts + (long long)la * lstride + lbc;  // element t at base + t*es
   const long long es = Bc;
@@ -602,7 +724,7 @@ __global__ void __launch_bounds__(NT) theta_fast_kernel(const ThetaParams p) {
 #pragma unroll
     for (int n1 = 0; n1 < M1; ++n1) {
       const int k = n2 + M2 * n1;
-      if (Bc == 1)
+      if (rows)
         keepa[q][n1] = __ldg(reinterpret_cast<const double2*>(p.X + base) + k);
       else
         keepa[q][n1] = make_double2(__ldg(p.X + base + (2LL * k) * es), __ldg(p.X + base + (2LL * k + 1) * es));
@@ -612,7 +734,9 @@ __global__ void __launch_bounds__(NT) theta_fast_kernel(const ThetaParams p) {
   for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, false>(keepa[q], S, lt + q * TPL, p.tw);
   const int cls = p.phi_class_a == 1 ? la : (p.phi_class_a == 0 ? lbc : la * Bc + lbc);
   const double* ph = p.phis + ((long long)c * p.nclass + cls) * p.phis_ld;
-  theta_tail<M1, M2, AXPY>(p, S, lt, ph, p.tw, f, base, es, Bc);
+  // contiguous lines (Bc == 1) keep a line's threads in consecutive lanes: register split
+  constexpr bool RS = ROWS && (TPL == M1) && ((TPL & (TPL - 1)) == 0) && TPL <= 32;
+  theta_tail<M1, M2, AXPY, false, RS, MODE>(p, S, lt, ph, p.tw, f, base, es, Bc);
 }
 
 }  // namespace cg
