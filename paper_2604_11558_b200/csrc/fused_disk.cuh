@@ -68,7 +68,14 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
   const long long fsz = sp.npts;  // disk plans are never padded here
   const uint32_t row_bytes = N * sizeof(double);
   constexpr int PS = D::PS;  // == tp.phis_ld (checked at plan set-up)
-  const uint32_t item_bytes = (uint32_t)(2 * (RPB + 2) * row_bytes + 2 * RPB * PS * sizeof(double));
+  const uint32_t w_bytes = (uint32_t)(2 * (RPB + 2) * row_bytes);
+  const uint32_t phi_bytes = (uint32_t)(2 * RPB * PS * sizeof(double));
+  // Phi rows depend on (operator set, row block) only: with shared operators
+  // (opb == 0) and a grid that is a multiple of the row blocks per run, a CTA
+  // sees the same row block in every item, so each buffer copies them once
+  int phi_rows[NBUF];
+#pragma unroll
+  for (int q = 0; q < NBUF; ++q) phi_rows[q] = -1;
 
 
   // copies of one item into buffer k (issued by one thread)
@@ -78,7 +85,9 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
     uint8_t* bb = bufs + k * D::buf;
     double* wst = reinterpret_cast<double*>(bb);
     double* phs = reinterpret_cast<double*>(bb + D::reg_a);
-    mbar_arrive_expect_tx(&full[k], item_bytes);
+    const bool load_phi = !(sp.opb == 0 && phi_rows[k] == i0);
+    phi_rows[k] = i0;
+    mbar_arrive_expect_tx(&full[k], w_bytes + (load_phi ? phi_bytes : 0u));
     const int lo = i0 > 0 ? i0 - 1 : 0;
     const int hi = (i0 + RPB < n1) ? i0 + RPB : n1 - 1;
     for (int comp = 0; comp < 2; ++comp) {
@@ -90,8 +99,9 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
                    &full[k]);
       if (i0 == 0) bulk_load_1d(dst, src, row_bytes, &full[k]);
       if (i0 + RPB >= n1) bulk_load_1d(dst + (size_t)(RPB + 1) * N, src + (long long)(n1 - 1) * N, row_bytes, &full[k]);
-      bulk_load_1d(phs + (size_t)comp * RPB * PS, tp.phis + ((long long)(b * sp.opb + comp) * tp.nclass + i0) * PS,
-                   (uint32_t)(RPB * PS * sizeof(double)), &full[k]);
+      if (load_phi)
+        bulk_load_1d(phs + (size_t)comp * RPB * PS, tp.phis + ((long long)(b * sp.opb + comp) * tp.nclass + i0) * PS,
+                     (uint32_t)(RPB * PS * sizeof(double)), &full[k]);
     }
   };
 
