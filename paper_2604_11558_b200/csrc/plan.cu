@@ -759,8 +759,11 @@ int launch_fused_nb(const ThetaParams& tp, const StencilParams& sp, cudaStream_t
   }
   const long long items = (long long)sp.batch * (sp.n1 / D::RPB);
   static const int cps = getenv("CURVIGPU_FRONT_CPS") ? std::max(1, atoi(getenv("CURVIGPU_FRONT_CPS"))) : 3 - NBUF;
-  const unsigned blocks =
-      (unsigned)std::min<long long>(items, (long long)num_sms * std::min(cps, 3 - NBUF) * (256 / NT));
+  static const int ctas_sm = getenv("CURVIGPU_FRONT_CTAS_PER_SM") ? atoi(getenv("CURVIGPU_FRONT_CTAS_PER_SM")) : 0;
+  // 128-thread CTAs: three per SM (3 x 63 KB of shared memory; measured best for config 5)
+  const long long per_sm = ctas_sm > 0 ? ctas_sm : (NT == 128 ? 3 : std::min(cps, 3 - NBUF) * (256 / NT));
+  static const int grid_env = getenv("CURVIGPU_FRONT_GRID") ? atoi(getenv("CURVIGPU_FRONT_GRID")) : 0;
+  const unsigned blocks = (unsigned)std::min<long long>(items, grid_env > 0 ? grid_env : (long long)num_sms * per_sm);
   int rc = launch_pdl(kern, dim3(blocks), dim3(NT), D::smem, s, tp, sp);
   if (rc) return rc;
   CUDA_TRY(cudaGetLastError());
@@ -771,6 +774,7 @@ template <int M1, int M2, int KIN>
 int launch_fused_t(const ThetaParams& tp, const StencilParams& sp, cudaStream_t s, bool configure_only, int nt) {
   static const int nbuf = getenv("CURVIGPU_FUSED_NBUF") ? atoi(getenv("CURVIGPU_FUSED_NBUF")) : 1;
   if (nt == 64) return launch_fused_nb<M1, M2, KIN, 1, 64>(tp, sp, s, configure_only);
+  if (nt == 128) return launch_fused_nb<M1, M2, KIN, 1, 128>(tp, sp, s, configure_only);
   if (nbuf == 1) return launch_fused_nb<M1, M2, KIN, 1>(tp, sp, s, configure_only);
   return launch_fused_nb<M1, M2, KIN, 2>(tp, sp, s, configure_only);
 }
@@ -876,6 +880,12 @@ int setup_fused_front(cg_plan* p) {
   const long long items256 = (long long)p->B * (p->n1 / (lpb / 2));
   if (items256 < sms && p->n1 % (lpb / 8) == 0 && (lpb / 8) % 2 == 0 && !getenv("CURVIGPU_NO_SMALL_CTA"))
     p->fused_nt = 64;
+  // enough items for three 128-thread CTAs per SM (config 5: 8192 items of 8 rows): 128-thread CTAs,
+  // front 163.2 -> 159.3 us against two 256-thread CTAs per SM (profiles/r01_front_variants.txt)
+  const long long items128 = (long long)p->B * (p->n1 / (lpb / 4));
+  if (p->fused_nt == 256 && items128 >= 3LL * sms && p->n1 % (lpb / 4) == 0 && (lpb / 4) % 2 == 0 &&
+      !getenv("CURVIGPU_FRONT_NT256"))
+    p->fused_nt = 128;
   if (getenv("CURVIGPU_FRONT_NT64") && p->n1 % (lpb / 8) == 0 && (lpb / 8) % 2 == 0) p->fused_nt = 64;  // measurement knob
   int rc = launch_fused_front(p, nullptr, false, nullptr, true);
   if (rc) return rc;
