@@ -409,7 +409,9 @@ def engine_arm(args):
     gemm_flops = sum(ens.plan.stage_info(s)[0] for s in range(ens.plan.stage_count()))
     # kernels one time step launches (fused front + GEMM in fft mode; launch list:
     # profiles/r01_v10_launches_summary.txt) x time steps, + the step-counter reset per cg_run
-    launches_per_step = chunk * len(ens.plan.step_kernels()) + 1
+    # with lanes every lane launches its own kernels (and its own step-counter reset)
+    lanes = ens.plan.lanes
+    launches_per_step = lanes * (chunk * len(ens.plan.step_kernels()) + 1)
     line = {
         "metric": METRIC,
         "value": value,
@@ -431,6 +433,7 @@ def engine_arm(args):
             "theta": args.theta + (" (exact real-FFT propagator for Q diag(Phi) Q^T)" if args.theta == "fft"
                                    else " (two DMMA mu-mode products, the reference's factorisation)"),
             "parallelism": f"ensemble shards over {world} GPU(s), no data-path collective",
+            "lanes": lanes,
             "l2": "state 268 MB/GPU at N=1 exceeds 126 MB L2; 256 MB L2 flush between timed bench steps",
         },
         "steps_per_s": chunk * args.steps / dev_sec,

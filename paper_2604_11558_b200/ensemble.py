@@ -133,14 +133,38 @@ class Ensemble:
         self.host_in.copy_(torch.as_tensor(np.ascontiguousarray(host_states)))
 
     def advance(self, nsteps: int, *, from_host: bool = True, to_host: bool = True):
-        """Optionally upload host_in, step nsteps, optionally download to host_out."""
+        """Optionally upload host_in, step nsteps, optionally download to host_out.
+
+        With a laned plan every lane uploads, steps and downloads its own run
+        block on its own stream, so lane 1's upload runs under lane 0's
+        stepping and lane 0's download under lane 1's tail."""
+        import torch
+
         if from_host:
-            self.state.copy_(self.host_in, non_blocking=True)
             self.first_bad.fill_(INT32_MAX)
+        lanes = self.plan.lane_blocks()
+        if not lanes:
+            if from_host:
+                self.state.copy_(self.host_in, non_blocking=True)
+            self.plan.run(self.state, 0 if from_host else self.step, nsteps, self.first_bad)
+        else:
+            cur = torch.cuda.current_stream()
+            ready = torch.cuda.Event()
+            ready.record(cur)
+            for lo, hi, sub, stream in lanes:
+                stream.wait_event(ready)
+                with torch.cuda.stream(stream):
+                    if from_host:
+                        self.state[lo:hi].copy_(self.host_in[lo:hi], non_blocking=True)
+                    sub.run(self.state[lo:hi], 0 if from_host else self.step, nsteps, self.first_bad[lo:hi])
+                    if to_host:
+                        self.host_out[lo:hi].copy_(self.state[lo:hi], non_blocking=True)
+            for _, _, _, stream in lanes:
+                cur.wait_stream(stream)
+        if from_host:
             self.step = 0
-        self.plan.run(self.state, self.step, nsteps, self.first_bad)
         self.step += nsteps
-        if to_host:
+        if to_host and not lanes:
             self.host_out.copy_(self.state, non_blocking=True)
         return self.host_out
 

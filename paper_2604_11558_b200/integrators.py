@@ -22,6 +22,7 @@ torch CUDA stream.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from enum import Enum
 from typing import Callable
@@ -261,12 +262,23 @@ class SplitPlan:
     ``(batch, ncomp, *grid)``, C-contiguous, reference axis order.
     """
 
+    # runs per lane below which a plan is not split into lanes (auto mode):
+    # each lane's kernels need several waves of work (profiles/r01_lanes.txt)
+    LANE_MIN_RUNS = 128
+
     def __init__(self, geos, batch: int = 1, kinetics: str = "external",
-                 kin_params=None, lifts=None, theta: str | None = None, ops_per_run: bool = False):
+                 kin_params=None, lifts=None, theta: str | None = None, ops_per_run: bool = False,
+                 lanes: int | None = None):
         """``geos``: one GeometryOps per component, shared by the ``batch``
         runs; with ``ops_per_run`` one per (run, component) in run-major
         order (a heterogeneous ensemble: runs may differ in coefficients and
-        domain sizes, the grid extents must agree)."""
+        domain sizes, the grid extents must agree).
+
+        ``lanes``: :meth:`run` advances the batch as that many independent
+        sub-plans on their own streams (contiguous run blocks; runs never
+        interact, so results are identical), which lets one lane's kernels
+        fill the other's ragged kernel tails.  ``None`` picks 2 for batches of
+        at least 2 * LANE_MIN_RUNS runs (env CURVIGPU_LANES overrides), else 1."""
         import torch  # noqa: F401  (device memory / streams)
 
         geos = list(geos)
@@ -353,11 +365,37 @@ class SplitPlan:
         handle = ctypes.c_void_p()
         _native.check(self._lib.cg_plan_create(ctypes.byref(d), ctypes.byref(handle)), "cg_plan_create")
         self._h = handle
+        # lanes: sub-plans over contiguous run blocks (run() only)
+        if lanes is None:
+            env = os.environ.get("CURVIGPU_LANES")
+            lanes = int(env) if env else (2 if self.batch >= 2 * self.LANE_MIN_RUNS else 1)
+        lanes = max(1, min(int(lanes), self.batch))
+        self._lanes = []
+        if lanes > 1:
+            kp_all = None if kin_params is None else _f64(kin_params).reshape(self.batch, -1)
+            cuts = [self.batch * k // lanes for k in range(lanes + 1)]
+            for lo, hi in zip(cuts[:-1], cuts[1:]):
+                sub_geos = geos[lo * C:hi * C] if ops_per_run else geos
+                sub = SplitPlan(sub_geos, batch=hi - lo, kinetics=kinetics,
+                                kin_params=None if kp_all is None else kp_all[lo:hi], lifts=lifts,
+                                theta=theta, ops_per_run=ops_per_run, lanes=1)
+                self._lanes.append((lo, hi, sub, torch.cuda.Stream()))
 
     def close(self):
+        for _, _, sub, _ in getattr(self, "_lanes", []):
+            sub.close()
+        self._lanes = []
         if getattr(self, "_h", None):
             self._lib.cg_plan_destroy(self._h)
             self._h = None
+
+    @property
+    def lanes(self) -> int:
+        return max(1, len(self._lanes))
+
+    def lane_blocks(self):
+        """[(lo, hi, sub_plan, stream)] of the lanes (empty for one lane)."""
+        return list(self._lanes)
 
     def __del__(self):
         try:
@@ -446,6 +484,20 @@ class SplitPlan:
         self._check_state(state, "state")
         if first_bad.dtype != torch.int32 or not first_bad.is_cuda or first_bad.numel() != self.batch * self.ncomp:
             raise ValueError("first_bad must be an int32 CUDA tensor with batch*ncomp entries")
+        if self._lanes:
+            # fork: every lane waits for the caller's stream, runs its run block
+            # on its own stream, and the caller's stream joins all lanes
+            cur = torch.cuda.current_stream()
+            ready = torch.cuda.Event()
+            ready.record(cur)
+            fb = first_bad.view(self.batch, self.ncomp)
+            for lo, hi, sub, stream in self._lanes:
+                stream.wait_event(ready)
+                with torch.cuda.stream(stream):
+                    sub.run(state[lo:hi], step0, nsteps, fb[lo:hi])
+            for _, _, _, stream in self._lanes:
+                cur.wait_stream(stream)
+            return
         _native.check(self._lib.cg_run(self._h, state.data_ptr(), int(step0), int(nsteps), first_bad.data_ptr(),
                                        self._stream()), "cg_run")
 

@@ -381,3 +381,49 @@ def test_fused_front_cta_variants_match_oracle_and_each_other(monkeypatch, theta
         globals()[key] = out
     else:
         assert np.array_equal(out, first)
+
+
+def test_lanes_give_identical_results(monkeypatch, theta_mode):
+    """A plan split into lanes (independent run blocks on their own streams)
+    equals the single plan bitwise, including the divergence record; the
+    Ensemble's per-lane upload / step / download path equals it too."""
+    import torch
+
+    from paper_2604_11558_b200.ensemble import Ensemble
+
+    ens = pcfg.config5_inputs(40, 12, SMALL[5])
+    params = np.stack([[g, 0.1, 0.9] for g in ens.gammas])
+    params[5, 0] = 5e8  # one member diverges: its first bad step must survive the lane split
+    outs = []
+    for lanes in (1, 2, 3):
+        plan = ensemble_plan_lanes(ens, params, lanes)
+        assert plan.lanes == lanes
+        state = torch.from_numpy(ens.states).cuda()
+        bad = torch.full((12, 2), INT32_MAX, dtype=torch.int32, device="cuda")
+        plan.run(state, 0, 30, bad)
+        outs.append((state.cpu().numpy(), bad.cpu().numpy()))
+        plan.close()
+    for o, b in outs[1:]:
+        assert np.array_equal(np.nan_to_num(o, nan=7.0), np.nan_to_num(outs[0][0], nan=7.0))
+        assert np.array_equal(b, outs[0][1])
+    assert (outs[0][1][5] < INT32_MAX).any() and (np.delete(outs[0][1], 5, axis=0) == INT32_MAX).all()
+    res = []
+    for lanes in ("1", "2"):
+        monkeypatch.setenv("CURVIGPU_LANES", lanes)
+        e = Ensemble(ens.template, "schnakenberg", params, 1e-3)
+        e.load(ens.states)
+        out = e.advance(30)
+        torch.cuda.synchronize()  # the download is asynchronous (pinned host buffer)
+        res.append((out.numpy().copy(), e.first_bad.cpu().numpy()))
+    assert np.array_equal(np.nan_to_num(res[0][0], nan=7.0), np.nan_to_num(res[1][0], nan=7.0))
+    assert np.array_equal(res[0][1], res[1][1])
+    assert np.array_equal(np.nan_to_num(res[0][0], nan=7.0), np.nan_to_num(outs[0][0], nan=7.0))
+
+
+def ensemble_plan_lanes(inputs, params, lanes):
+    from paper_2604_11558_b200.integrators import SplitPlan, prepare
+
+    geos = [prepare(c.ops, 1e-3) for c in inputs.template.components]
+    lifts = [float(c.lift) for c in inputs.template.components]
+    return SplitPlan(geos, batch=params.shape[0], kinetics="schnakenberg", kin_params=params, lifts=lifts,
+                     lanes=lanes)
