@@ -485,6 +485,17 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
   constexpr int M = F::M, TPL = F::TPL;
   constexpr int RMAX = M1 > M2 ? M1 : M2;
   double2 r[RMAX];
+  // column lines with the axpy epilogue (the sphere: few, latency-bound CTAs)
+  // issue their W loads before the whole tail, so they land under the FFT
+  constexpr bool EARLY = AXPY && BCM == 2 && M1 / TPL == 1;
+  double2 wearly[EARLY ? M2 : 1];
+  if constexpr (EARLY) {
+#pragma unroll
+    for (int k2 = 0; k2 < M2; ++k2) {
+      const long long o0 = base + (2LL * (lt + M1 * k2)) * es;
+      wearly[k2] = make_double2(__ldg(p.Wprev + o0), __ldg(p.Wprev + o0 + es));
+    }
+  }
   __syncthreads();
   if constexpr (RS) {
     static_assert(TPL == M1 && (TPL & (TPL - 1)) == 0 && TPL <= 32 && M2 % 2 == 0, "register split layout");
@@ -624,7 +635,10 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
   for (int q = 0; q < M1 / TPL; ++q) {
     const int k1 = lt + q * TPL;
     double2 wpre[PRE ? M2 : 1];
-    if constexpr (PRE) {
+    if constexpr (EARLY) {
+#pragma unroll
+      for (int k2 = 0; k2 < M2; ++k2) wpre[k2] = wearly[k2];
+    } else if constexpr (PRE) {
 #pragma unroll
       for (int k2 = 0; k2 < M2; ++k2) {
         const int k = k1 + M1 * k2;
