@@ -21,14 +21,26 @@
 // Epilogues are fused: plain store, Hadamard with a phi1 tensor (the "T *=
 // Phi" of the steppers), or the final "W + tau * T" with the divergence
 // guard of run_simulation (integrators.py:422-427).
+//
+// EPI_CHAIN (TN only, N = K <= BN): two products along the same mode in one
+// pass, Y = ((X . B1^T) o Phi) . B2^T -- the ball's "T = F x3 V^-1 o Phi;
+// T = T x3 V" (integrators.py:217-226).  A tile covers all N columns: after
+// the first k loop the Phi-scaled accumulators go into the shared-memory
+// tile (in the 128B-swizzled k-slice layout the TMA gives the A operand),
+// the producer streams B2 (passed as mapW) slices into the same ring and
+// the second k loop reads A from that tile.  The intermediate never goes to
+// HBM; DMMAs on column blocks >= N and k steps >= K are skipped (they only
+// add zeros), so n = 100 costs 104 x 100 instead of 128 x 112 per row.
 #pragma once
+
+#include <type_traits>
 
 #include "common.cuh"
 
 namespace cg {
 
 enum { VAR_TN = 0, VAR_NN = 1 };
-enum { EPI_STORE = 0, EPI_PHI = 1, EPI_AXPY = 2 };
+enum { EPI_STORE = 0, EPI_PHI = 1, EPI_AXPY = 2, EPI_CHAIN = 3 };
 
 struct GemmParams {
   int M, N, K;
@@ -64,6 +76,12 @@ constexpr int gemm_smem_bytes() {
 // Row permutation within an 8-row group used by the TN fragments: rows of a
 // half-warp land on distinct 128B-swizzle phases.
 __device__ __forceinline__ int perm8(int g) { return ((g & 3) << 1) | (g >> 2); }
+// Row -> 16-byte-chunk XOR of the EPI_CHAIN intermediate tile (bits 1 and 2 of
+// the row swapped): the epilogue's 16-byte stores (quarter-warps = row pairs
+// r, r^2) and the second k loop's 8-byte fragment loads (half-warps = rows
+// {0,2,4,6} / {1,3,5,7}) both hit distinct bank groups.  The TMA 128B swizzle
+// (XOR = row) gave the stores 2-way conflicts per quarter-warp.
+__device__ __forceinline__ int chain_xor(int r) { return (r & 1) | ((r & 2) << 1) | ((r & 4) >> 1); }
 
 // mapA / mapB: operand tensor maps (128B swizzle).  mapW: previous state,
 // mapO: output, both viewed as (N, M, slab, field) with a (BN, BM) box; the
@@ -88,6 +106,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
   constexpr int SA = StageBytes<BM, BN>::A, SB = StageBytes<BM, BN>::B;
   constexpr int STAGE = SA + SB;
   constexpr int EPIB = StageBytes<BM, BN>::epi;
+  static_assert(EPI != EPI_CHAIN || (VAR == VAR_TN && KS == 1), "chained products: TN, one CTA per tile");
 
   extern __shared__ uint8_t smem_raw[];
   // align by pointer arithmetic on the shared array (an integer round trip
@@ -154,7 +173,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
       int pm0 = 0, pn0 = 0, ps = 0, pf = 0;  // previous tile (pending store)
       auto store_prev = [&](int ptc) {
         mbar_wait(epi_ready, ptc & 1);
-        if ((pm0 + BM <= p.M) && (pn0 + BN <= p.N)) {  // partial tiles were stored from registers
+        // partial tiles (and every CHAIN tile: etile holds its intermediate) were stored from registers
+        if (EPI != EPI_CHAIN && (pm0 + BM <= p.M) && (pn0 + BN <= p.N)) {
           tma_store_4d(&mapO, etile, pn0, pm0, ps, pf);
           bulk_commit();
         }
@@ -169,13 +189,20 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
         const int c = f % p.ncomp;
         const int m0 = tm * BM, n0 = tn * BN;
         const int kb = KS > 1 ? kt_begin : 0, ke = KS > 1 ? kt_end : KT;
-        const int kstore = kb + (ke - kb < STAGES ? ke - kb : STAGES);  // slices issued before the previous store
-        for (int kt = kb; kt < ke; ++kt, ++it) {
-          if (rank == 0 && tc > 0 && kt == kstore) store_prev(tc - 1);
+        const int qe = EPI == EPI_CHAIN ? ke + (ke - kb) : ke;  // CHAIN: then the B2 slices
+        const int kstore = kb + (qe - kb < STAGES ? qe - kb : STAGES);  // slices issued before the previous store
+        for (int q = kb; q < qe; ++q, ++it) {
+          if (rank == 0 && tc > 0 && q == kstore) store_prev(tc - 1);
           const int st = it % STAGES;
           if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
           uint8_t* sa = smem + st * STAGE;
           uint8_t* sb = sa + SA;
+          if (EPI == EPI_CHAIN && q >= ke) {
+            mbar_arrive_expect_tx(&full[st], SB);
+            tma_load_3d(sb, &mapW, &full[st], (q - ke) * 16, n0, c);
+            continue;
+          }
+          const int kt = q;
           mbar_arrive_expect_tx(&full[st], STAGE);
           if (VAR == VAR_TN) {
             tma_load_3d(sa, &mapA, &full[st], kt * 16, m0, f);
@@ -189,7 +216,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
         }
         if (rank == 0) {
           if (tc > 0) {
-            if (kstore == ke) store_prev(tc - 1);
+            if (kstore == qe) store_prev(tc - 1);
             bulk_wait_read0();      // the previous tile's store has read etile
             mbar_arrive(epi_empty);
           }
@@ -223,6 +250,63 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
   if (EPI == EPI_AXPY) step_now = *p.step;
   int it = 0, tc = 0;
 
+  // EPI_CHAIN: Phi for chain_mid, loaded when the tile starts (its L2 latency
+  // hides under the first k loop)
+  auto chain_phi = [&](double2 (&ph)[MT][NT], int cc, int ss, int mb, int wm, int wn, int gg, int tqq) {
+    const int cin8 = ((tqq & 1) << 2) | (tqq & 2);
+    const int rin8 = perm8(gg);
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int ml = wm + i * 8 + rin8;
+      const int m = mb + ml < p.M ? mb + ml : 0;
+      const double* phirow = p.phi + cc * p.phi_c + ss * p.phi_s + (long long)(m / p.phi_rdiv) * p.phi_m;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int n = wn + j * 8 + cin8;
+        const int nlo = n < p.N ? n : 0;
+        const int nhi = n + 1 < p.N ? n + 1 : nlo;
+        ph[i][j].x = __ldg(phirow + (long long)nlo * p.phi_n);
+        ph[i][j].y = __ldg(phirow + (long long)nhi * p.phi_n);
+      }
+    }
+  };
+  // EPI_CHAIN, between the two k loops: the first product's accumulators,
+  // times Phi, become the second product's A operand in etile ([KT][BM][16]
+  // k slices, rows XOR-swizzled by chain_xor); accumulators reset.
+  auto chain_mid = [&](double (&ac)[MT][NT][2], const double2 (&ph)[MT][NT], int tcn, int wm, int wn, int gg,
+                       int tqq) {
+    // No epi_empty wait here: the producer only signals it after issuing all
+    // 2 KT slices of this tile, which needs this tile's second loop to drain
+    // the ring (deadlock).  Nothing async touches etile in CHAIN mode (every
+    // tile is stored from registers, there is no W tile), and the previous
+    // tile's second loop finished reading it before the closing named barrier.
+    (void)tcn;
+    const int cin8 = ((tqq & 1) << 2) | (tqq & 2);
+    const int rin8 = perm8(gg);
+    const int kcols = KT * 16;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int ml = wm + i * 8 + rin8;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        // TN fragments hold columns perm8(2t), perm8(2t+1): swap with lane^2 into adjacent pairs
+        const bool hi = (tqq & 2) != 0;
+        const double send = hi ? ac[i][j][0] : ac[i][j][1];
+        const double recv = __shfl_xor_sync(0xffffffffu, send, 2);
+        double v0 = hi ? recv : ac[i][j][0];
+        double v1 = hi ? ac[i][j][1] : recv;
+        ac[i][j][0] = ac[i][j][1] = 0.0;
+        const int n = wn + j * 8 + cin8;
+        if (n >= kcols) continue;
+        v0 *= ph[i][j].x;
+        v1 *= ph[i][j].y;
+        double* slab = etile + (n >> 4) * (BM * 16) + ml * 16;
+        *reinterpret_cast<double2*>(slab + (((((n & 15) >> 1) ^ chain_xor(ml & 7))) << 1)) = make_double2(v0, v1);
+      }
+    }
+    named_bar(1, NCW * 32);  // the whole intermediate tile is written before any warp reads it
+  };
+
   for (int tile = KS > 1 ? cid : (int)blockIdx.x; tile < ntiles; tile += KS > 1 ? ncl : (int)gridDim.x, ++tc) {
     int r = tile;
     const int tn = r % p.tiles_n;
@@ -239,30 +323,61 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
 #pragma unroll
       for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    for (int kt = KS > 1 ? kt_begin : 0; kt < (KS > 1 ? kt_end : KT); ++kt, ++it) {
+    double2 phc[MT][NT];
+    if constexpr (EPI == EPI_CHAIN) chain_phi(phc, c, s, m0, wm0, wn0, g, tq);
+    const int kend = KS > 1 ? kt_end : KT;
+    const int qend = EPI == EPI_CHAIN ? 2 * KT : kend;
+    for (int q = KS > 1 ? kt_begin : 0; q < qend; ++q, ++it) {
+      if (EPI == EPI_CHAIN && q == KT) chain_mid(acc, phc, tc, wm0, wn0, g, tq);
+      const int kt = (EPI == EPI_CHAIN && q >= KT) ? q - KT : q;
       const int st = it % STAGES;
       mbar_wait(&full[st], (it / STAGES) & 1);
       // mma.sync.aligned needs the whole warp converged: lanes leave the
       // try_wait poll independently, and lane 0 may still be in the
       // previous tile's store block
       __syncwarp();
-      const double* sa = reinterpret_cast<const double*>(smem + st * STAGE);
+      const double* sa = (EPI == EPI_CHAIN && q >= KT) ? etile + kt * BM * 16
+                                                        : reinterpret_cast<const double*>(smem + st * STAGE);
       const double* sb = reinterpret_cast<const double*>(smem + st * STAGE + SA);
       if (VAR == VAR_TN) {
         const int pg = perm8(g);
+        const int pga = (EPI == EPI_CHAIN && q >= KT) ? chain_xor(pg) : pg;  // A from the intermediate tile
+        // CHAIN: k steps past K and column blocks past N only add zeros.  The
+        // skips are warp-uniform branches to code with a compile-time count of
+        // live column blocks NL (predicated-off DMMAs would still issue).
+        const int kmax = EPI == EPI_CHAIN ? min(16, p.K - kt * 16) : 16;
+        auto slice = [&](auto nlive) {
+          constexpr int NL = decltype(nlive)::value;
 #pragma unroll
-        for (int kk = 0; kk < 16; kk += 4) {
-          const int col = kk + tq;
-          const int off = ((((col >> 1) ^ pg)) << 1) | (col & 1);
-          double a[MT], b[NT];
+          for (int kk = 0; kk < 16; kk += 4) {
+            if (EPI == EPI_CHAIN && kk >= kmax) break;
+            const int col = kk + tq;
+            const int off = ((((col >> 1) ^ pg)) << 1) | (col & 1);
+            const int offa = ((((col >> 1) ^ pga)) << 1) | (col & 1);
+            double a[MT], b[NL];
 #pragma unroll
-          for (int i = 0; i < MT; ++i) a[i] = sa[(wm0 + i * 8 + pg) * 16 + off];
+            for (int i = 0; i < MT; ++i) a[i] = sa[(wm0 + i * 8 + pg) * 16 + offa];
 #pragma unroll
-          for (int j = 0; j < NT; ++j) b[j] = sb[(wn0 + j * 8 + pg) * 16 + off];
+            for (int j = 0; j < NL; ++j) b[j] = sb[(wn0 + j * 8 + pg) * 16 + off];
 #pragma unroll
-          for (int i = 0; i < MT; ++i)
+            for (int i = 0; i < MT; ++i)
 #pragma unroll
-            for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+              for (int j = 0; j < NL; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+          }
+        };
+        if constexpr (EPI == EPI_CHAIN) {
+          static_assert(NT == 4, "chain tile: four 8-column blocks per warp");
+          const int nl = (p.N - wn0 + 7) >> 3;  // live column blocks of this warp
+          if (nl >= 4)
+            slice(std::integral_constant<int, 4>{});
+          else if (nl == 3)
+            slice(std::integral_constant<int, 3>{});
+          else if (nl == 2)
+            slice(std::integral_constant<int, 2>{});
+          else if (nl == 1)
+            slice(std::integral_constant<int, 1>{});
+        } else {
+          slice(std::integral_constant<int, NT>{});
         }
       } else {
 #pragma unroll
@@ -372,14 +487,15 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
 
     if (EPI == EPI_AXPY)
       mbar_wait(epi_full, tc & 1);  // W tile is in etile
-    else if (tc > 0)
+    else if (EPI != EPI_CHAIN && tc > 0)
       mbar_wait(epi_empty, (tc - 1) & 1);  // previous tile's store has read etile
     bool bad = false;
     // Partial tiles (the last m or n tile of an extent that BM/BN do not
     // divide) are written straight from registers with bounds checks: the
     // clipped bulk tensor store of such tiles measured nondeterministic on
     // B200 with two CTAs per SM (tools/chain_dbg2.py); full tiles use TMA.
-    const bool full_tile = (m0 + BM <= p.M) && (n0 + BN <= p.N);
+    // CHAIN: etile holds the intermediate other warps may still be reading
+    const bool full_tile = EPI != EPI_CHAIN && (m0 + BM <= p.M) && (n0 + BN <= p.N);
     // Phi1 operands for EPI_PHI (L2-resident table), all loads in flight per row group
     constexpr int EC = (MINB >= 2 && MT > 2) ? MT / 2 : MT;
 #pragma unroll

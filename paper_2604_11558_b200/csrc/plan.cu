@@ -117,13 +117,14 @@ int make_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
 struct TileCfg {
   int BM, BN;
 };
-constexpr int kNumCfg = 14;
+constexpr int kNumCfg = 15;
+constexpr int kChainCfg = 14;  // EPI_CHAIN only: 32 rows x all (<= 128) columns, 8 warps of 16x32
 // 7, 8: the 64x64 configuration split-K over clusters of 2 / 4 CTAs
 // 9, 10: 64x64 tiles on 8 consumer warps (32x16 / 16x32 warp tiles); 11: 10 split-K over 2-CTA clusters
 // 12: 32x32 tiles on 4 warps of 16x16 (stages with very few 64x64 tiles); 13: 12 split-K over 2-CTA clusters
 constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {64, 128}, {128, 128}, {64, 64},
                                     {64, 64}, {64, 64}, {64, 64}, {64, 64}, {64, 64},
-                                    {32, 32}, {32, 32}};
+                                    {32, 32}, {32, 32}, {32, 128}};
 
 // BM, BN, warp tile, stages; 32x32 warp tiles keep the accumulators +
 // fragments under ~160 registers without spills.
@@ -138,6 +139,7 @@ constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {
 #define CFG9 64, 64, 32, 16, 4, 2
 #define CFG10 64, 64, 16, 32, 4, 2
 #define CFG12 32, 32, 16, 16, 4, 4
+#define CFG14 32, 128, 16, 32, 3, 2
 
 // configure_only: set the dynamic shared memory opt-in (done at plan
 // creation, never inside a stream capture).  KS > 1 launches clusters of KS
@@ -241,6 +243,10 @@ int launch_gemm_cfg(int cfg, const Maps& m, const GemmParams& p, cudaStream_t st
 }
 
 int launch_gemm(int var, int epi, int cfg, const Maps& m, const GemmParams& p, cudaStream_t s, bool conf = false) {
+  if (epi == EPI_CHAIN) {  // m.w carries the second operator's map
+    if (var != VAR_TN || cfg != kChainCfg) return fail(CG_EINVAL, "chained stage needs the TN chain tile");
+    return launch_gemm_t<VAR_TN, CFG14, EPI_CHAIN>(m.a, m.b, m.w, m.o, p, s, conf);
+  }
   if (var == VAR_TN) {
     if (epi == EPI_STORE) return launch_gemm_cfg<VAR_TN, EPI_STORE>(cfg, m, p, s, conf);
     if (epi == EPI_PHI) return launch_gemm_cfg<VAR_TN, EPI_PHI>(cfg, m, p, s, conf);
@@ -325,6 +331,7 @@ struct Stage {
   long long phi_c, phi_s;
   int phi_m, phi_n, phi_rdiv;
   CUtensorMap opmap;  // operator operand (B for TN, A for NN)
+  CUtensorMap opmap2;  // EPI_CHAIN: the second operator (B2, TN layout)
   // VAR_THETA: field = [A][N][Bc], W lines per CTA, Phi_j table, twiddles
   int tA, tBc, tW, tclass_mode, tnclass;
   const double* phif;
@@ -425,7 +432,7 @@ int pick_cfg(int var, long long nbatch, int M, int N, int K, int stage_index) {
       if (*q == ',') ++q;
     }
     const int v = nv == 1 ? vals[0] : (stage_index < nv ? vals[stage_index] : -1);
-    if (v >= 0 && v < kNumCfg) return v;
+    if (v >= 0 && v < kChainCfg) return v;
   }
   // Measured on B200 with the TMA epilogue (tools/sweep_tiles.py,
   // profiles/r01_tile_sweep_tmaepi.txt): 64x64 tiles, 4-stage ring, 2 CTAs/SM
@@ -462,7 +469,8 @@ int pick_cfg(int var, long long nbatch, int M, int N, int K, int stage_index) {
 
 // Build one GEMM stage: operator L (n x n) via `get`, shapes, epilogue.
 template <typename Get>
-int add_stage(cg_plan* p, int var, int epi, int M, int N, int K, int nslab, int src, int dst, int n_op, Get get) {
+int add_stage(cg_plan* p, int var, int epi, int M, int N, int K, int nslab, int src, int dst, int n_op, Get get,
+              int force_cfg = -1) {
   Stage st{};
   st.var = var;
   st.epi = epi;
@@ -481,7 +489,7 @@ int add_stage(cg_plan* p, int var, int epi, int M, int N, int K, int nslab, int 
     st.ldr = st.N;
   }
   const long long nbatch = (long long)p->B * p->C * nslab;
-  st.cfg = pick_cfg(var, nbatch, M, N, K, (int)p->stages.size());
+  st.cfg = force_cfg >= 0 ? force_cfg : pick_cfg(var, nbatch, M, N, K, (int)p->stages.size());
   double* op = nullptr;
   const int box_rows = (var == VAR_TN) ? kCfgs[st.cfg].BN : 16;
   int rc = upload_operator(p, var, n_op, get, &op, &st.opmap, box_rows);
@@ -730,6 +738,8 @@ int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
       if ((rc = make_map(&mp.o, dst, 4, dims, strides, box, false))) return rc;
       if (st.epi == EPI_AXPY) {
         if ((rc = make_map(&mp.w, Win, 4, dims, strides, box, false))) return rc;
+      } else if (st.epi == EPI_CHAIN) {
+        mp.w = st.opmap2;
       } else {
         mp.w = mp.o;
       }
@@ -939,6 +949,35 @@ int build_stages(cg_plan* p, const cg_desc* d) {
     return add_stage(p, VAR_NN, EPI_AXPY, n1, n2 * n3, n1, 1, BUF_X, BUF_OUT, n1,
                      [&](int c, int r, int q) { return P1[((size_t)c * n1 + r) * n1 + q]; });
   }
+  // Ball, polar (last) mode: T = (F x3 V^-1) o Phi_outer, T = T x3 V
+  // (integrators.py:217-226).  Both products run in one chained kernel
+  // (gemm.cuh EPI_CHAIN, the intermediate stays in shared memory) when the
+  // mode fits one 128-column tile; CURVIGPU_NO_CHAIN keeps two stages
+  // (bitwise-identical results, tests/test_gpu_parity.py).  Returns the
+  // buffer holding T.
+  auto ball_polar_mode = [&](double* phio, int* cur) -> int {
+    const double *V = d->V_phi, *Vi = d->Vinv_phi;
+    auto get_vi = [&](int c, int r, int q) { return Vi[((size_t)c * n3 + r) * n3 + q]; };
+    auto get_v = [&](int c, int r, int q) { return V[((size_t)c * n3 + r) * n3 + q]; };
+    const bool chain = n3 <= kCfgs[kChainCfg].BN && !getenv("CURVIGPU_NO_CHAIN");
+    int r2 = chain ? add_stage(p, VAR_TN, EPI_CHAIN, n1 * n2, n3, n3, 1, BUF_X, BUF_Y, n3, get_vi, kChainCfg)
+                   : add_stage(p, VAR_TN, EPI_PHI, n1 * n2, n3, n3, 1, BUF_X, BUF_Y, n3, get_vi);
+    if (r2) return r2;
+    Stage& s0 = p->stages.back();
+    s0.phi = phio;
+    s0.phi_c = (long long)n1 * n3;
+    s0.phi_rdiv = n2;
+    s0.phi_m = n3;
+    s0.phi_n = 1;
+    if (chain) {
+      double* op2 = nullptr;
+      *cur = BUF_Y;
+      return upload_operator(p, VAR_TN, n3, get_v, &op2, &s0.opmap2, kCfgs[kChainCfg].BN);
+    }
+    *cur = BUF_X;
+    return add_stage(p, VAR_TN, EPI_STORE, n1 * n2, n3, n3, 1, BUF_Y, BUF_X, n3, get_v);
+  };
+  auto other = [](int b) { return b == BUF_X ? BUF_Y : BUF_X; };
   if (p->geom == CG_BALL && fft && fft_extent(n2)) {
     if ((rc = need(d->phi1_rho, "phi1_rho")) || (rc = need(d->Phi, "Phi")) ||
         (rc = need(d->Phi_outer, "Phi_outer")) || (rc = need(d->V_phi, "V_phi")) ||
@@ -946,25 +985,15 @@ int build_stages(cg_plan* p, const cg_desc* d) {
       return rc;
     double* phio = nullptr;
     if ((rc = up_phi(d->Phi_outer, (size_t)n1 * n3, &phio))) return rc;
-    const double *V = d->V_phi, *Vi = d->Vinv_phi, *P1 = d->phi1_rho, *Ph = d->Phi;
-    if ((rc = add_stage(p, VAR_TN, EPI_PHI, n1 * n2, n3, n3, 1, BUF_X, BUF_Y, n3,
-                        [&](int c, int r, int q) { return Vi[((size_t)c * n3 + r) * n3 + q]; })))
-      return rc;
-    Stage& s0 = p->stages.back();
-    s0.phi = phio;
-    s0.phi_c = (long long)n1 * n3;
-    s0.phi_rdiv = n2;
-    s0.phi_m = n3;
-    s0.phi_n = 1;
-    if ((rc = add_stage(p, VAR_TN, EPI_STORE, n1 * n2, n3, n3, 1, BUF_Y, BUF_X, n3,
-                        [&](int c, int r, int q) { return V[((size_t)c * n3 + r) * n3 + q]; })))
-      return rc;
-    if ((rc = add_theta_stage(p, EPI_STORE, BUF_X, BUF_Y, n2, n1, n3, 2, n1 * n3, [&](int c, int cls, int col) {
+    const double *P1 = d->phi1_rho, *Ph = d->Phi;
+    int cur = BUF_X;
+    if ((rc = ball_polar_mode(phio, &cur))) return rc;
+    if ((rc = add_theta_stage(p, EPI_STORE, cur, other(cur), n2, n1, n3, 2, n1 * n3, [&](int c, int cls, int col) {
            const int i = cls / n3, k = cls % n3;
            return Ph[(((size_t)c * n1 + i) * n2 + col) * n3 + k];
          })))
       return rc;
-    return add_stage(p, VAR_NN, EPI_AXPY, n1, n2 * n3, n1, 1, BUF_Y, BUF_OUT, n1,
+    return add_stage(p, VAR_NN, EPI_AXPY, n1, n2 * n3, n1, 1, other(cur), BUF_OUT, n1,
                      [&](int c, int r, int q) { return P1[((size_t)c * n1 + r) * n1 + q]; });
   }
   if (p->geom == CG_DISK) {
@@ -1021,23 +1050,13 @@ int build_stages(cg_plan* p, const cg_desc* d) {
     double *phi = nullptr, *phio = nullptr;
     if ((rc = up_phi(d->Phi, (size_t)n1 * n2 * n3, &phi))) return rc;
     if ((rc = up_phi(d->Phi_outer, (size_t)n1 * n3, &phio))) return rc;
-    const double *V = d->V_phi, *Vi = d->Vinv_phi, *P1 = d->phi1_rho;
-    // T = F x3 V^-1, epilogue *= Phi_outer_c(i, k)
-    if ((rc = add_stage(p, VAR_TN, EPI_PHI, n1 * n2, n3, n3, 1, BUF_X, BUF_Y, n3,
-                        [&](int c, int r, int q) { return Vi[((size_t)c * n3 + r) * n3 + q]; })))
-      return rc;
-    Stage& s0 = p->stages.back();
-    s0.phi = phio;
-    s0.phi_c = (long long)n1 * n3;
-    s0.phi_rdiv = n2;
-    s0.phi_m = n3;
-    s0.phi_n = 1;
-    // T = T x3 V
-    if ((rc = add_stage(p, VAR_TN, EPI_STORE, n1 * n2, n3, n3, 1, BUF_Y, BUF_X, n3,
-                        [&](int c, int r, int q) { return V[((size_t)c * n3 + r) * n3 + q]; })))
-      return rc;
+    const double* P1 = d->phi1_rho;
+    // T = (F x3 V^-1) o Phi_outer_c(i, k), T = T x3 V
+    int cur = BUF_X;
+    if ((rc = ball_polar_mode(phio, &cur))) return rc;
+    const int b0 = cur, b1 = other(cur);
     // T = T x2 Q^T, epilogue *= Phi_c(i, j, k)
-    if ((rc = add_stage(p, VAR_NN, EPI_PHI, n2, n3, n2, n1, BUF_X, BUF_Y, n2,
+    if ((rc = add_stage(p, VAR_NN, EPI_PHI, n2, n3, n2, n1, b0, b1, n2,
                         [&](int c, int r, int q) { return Q[((size_t)c * n2 + q) * n2 + r]; })))
       return rc;
     Stage& s2 = p->stages.back();
@@ -1047,11 +1066,11 @@ int build_stages(cg_plan* p, const cg_desc* d) {
     s2.phi_m = n3;
     s2.phi_n = 1;
     // T = T x2 Q
-    if ((rc = add_stage(p, VAR_NN, EPI_STORE, n2, n3, n2, n1, BUF_Y, BUF_X, n2,
+    if ((rc = add_stage(p, VAR_NN, EPI_STORE, n2, n3, n2, n1, b1, b0, n2,
                         [&](int c, int r, int q) { return Q[((size_t)c * n2 + r) * n2 + q]; })))
       return rc;
     // W + tau * (T x1 phi1_rho)
-    if ((rc = add_stage(p, VAR_NN, EPI_AXPY, n1, n2 * n3, n1, 1, BUF_X, BUF_OUT, n1,
+    if ((rc = add_stage(p, VAR_NN, EPI_AXPY, n1, n2 * n3, n1, 1, b0, BUF_OUT, n1,
                         [&](int c, int r, int q) { return P1[((size_t)c * n1 + r) * n1 + q]; })))
       return rc;
   } else {  // cylinder
@@ -1273,7 +1292,7 @@ int cg_plan_stage_info(const cg_plan* p, int stage, long long* flops, long long*
   }
   const Stage& st = p->stages[stage];
   const long long items = (long long)p->B * p->C * st.nslab;
-  if (flops) *flops = 2LL * st.M * st.N * st.K * items;
+  if (flops) *flops = (st.epi == EPI_CHAIN ? 4LL : 2LL) * st.M * st.N * st.K * items;  // a chain is two products
   if (bytes) *bytes = (st.epi == EPI_AXPY ? 3LL : 2LL) * p->elems_u * (long long)sizeof(double);
   return CG_OK;
 }

@@ -427,3 +427,39 @@ def ensemble_plan_lanes(inputs, params, lanes):
     lifts = [float(c.lift) for c in inputs.template.components]
     return SplitPlan(geos, batch=params.shape[0], kinetics="schnakenberg", kin_params=params, lifts=lifts,
                      lanes=lanes)
+
+
+@pytest.mark.parametrize("dims", [(8, 16, 10), (5, 6, 7), (6, 8, 128), (100, 100, 100)])
+def test_ball_chained_polar_products_match_two_stages_bitwise(monkeypatch, theta_mode, dims):
+    """The ball's two polar-mode products (x3 V^-1, o Phi_outer, x3 V) run as
+    one chained kernel (intermediate in shared memory, zero column blocks
+    and k steps skipped) and, under CURVIGPU_NO_CHAIN, as two GEMM stages:
+    the plans differ by one stage and give bitwise-equal fields after 25
+    steps (odd n3 = 7: padded rows; n3 = 128: the chain tile's full width);
+    the chained run also matches the oracle."""
+    import torch
+
+    sysm = pcfg.BUILDERS[4](dims)
+    tau = 1e-2
+    geos = [prepare(c.ops, tau) for c in sysm.components]
+    kin = sysm.kinetics
+    W0 = torch.from_numpy(np.stack([c.initial for c in sysm.components])[None]).cuda()
+    outs, nstages = [], []
+    for chain in (True, False):
+        if chain:
+            monkeypatch.delenv("CURVIGPU_NO_CHAIN", raising=False)
+        else:
+            monkeypatch.setenv("CURVIGPU_NO_CHAIN", "1")
+        plan = SplitPlan(geos, 1, kin.kind, kin.param_vector()[None, :], theta=theta_mode)
+        nstages.append(plan.stage_count())
+        s = W0.clone()
+        bad = torch.full((1, 2), INT32_MAX, dtype=torch.int32, device="cuda")
+        plan.run(s, 0, 25, bad)
+        outs.append(s.cpu().numpy())
+    assert nstages[0] == nstages[1] - 1
+    assert np.array_equal(outs[0], outs[1])
+    if dims != (100, 100, 100):
+        osys = ocfg.BUILDERS[4](dims, initial=[c.initial for c in sysm.components])
+        ref = orc.integrate(osys, 25, 25 * tau)
+        for i, c in enumerate(sysm.components):
+            assert rel_inf(outs[0][0, i], ref[c.name]) <= STEP1_TOL, c.name
