@@ -117,14 +117,15 @@ int make_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
 struct TileCfg {
   int BM, BN;
 };
-constexpr int kNumCfg = 15;
+constexpr int kNumCfg = 16;
 constexpr int kChainCfg = 14;  // EPI_CHAIN only: 32 rows x all (<= 128) columns, 8 warps of 16x32
+constexpr int kChainCfg16 = 15;  // EPI_CHAIN, 16-row tiles on 4 warps at 3 CTAs/SM (CURVIGPU_CHAIN_CFG=15)
 // 7, 8: the 64x64 configuration split-K over clusters of 2 / 4 CTAs
 // 9, 10: 64x64 tiles on 8 consumer warps (32x16 / 16x32 warp tiles); 11: 10 split-K over 2-CTA clusters
 // 12: 32x32 tiles on 4 warps of 16x16 (stages with very few 64x64 tiles); 13: 12 split-K over 2-CTA clusters
 constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {64, 128}, {128, 128}, {64, 64},
                                     {64, 64}, {64, 64}, {64, 64}, {64, 64}, {64, 64},
-                                    {32, 32}, {32, 32}, {32, 128}};
+                                    {32, 32}, {32, 32}, {32, 128}, {16, 128}};
 
 // BM, BN, warp tile, stages; 32x32 warp tiles keep the accumulators +
 // fragments under ~160 registers without spills.
@@ -140,6 +141,7 @@ constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {
 #define CFG10 64, 64, 16, 32, 4, 2
 #define CFG12 32, 32, 16, 16, 4, 4
 #define CFG14 32, 128, 16, 32, 3, 2
+#define CFG15 16, 128, 16, 32, 3, 3
 
 // configure_only: set the dynamic shared memory opt-in (done at plan
 // creation, never inside a stream capture).  KS > 1 launches clusters of KS
@@ -244,7 +246,9 @@ int launch_gemm_cfg(int cfg, const Maps& m, const GemmParams& p, cudaStream_t st
 
 int launch_gemm(int var, int epi, int cfg, const Maps& m, const GemmParams& p, cudaStream_t s, bool conf = false) {
   if (epi == EPI_CHAIN) {  // m.w carries the second operator's map
-    if (var != VAR_TN || cfg != kChainCfg) return fail(CG_EINVAL, "chained stage needs the TN chain tile");
+    if (var != VAR_TN || (cfg != kChainCfg && cfg != kChainCfg16))
+      return fail(CG_EINVAL, "chained stage needs a TN chain tile");
+    if (cfg == kChainCfg16) return launch_gemm_t<VAR_TN, CFG15, EPI_CHAIN>(m.a, m.b, m.w, m.o, p, s, conf);
     return launch_gemm_t<VAR_TN, CFG14, EPI_CHAIN>(m.a, m.b, m.w, m.o, p, s, conf);
   }
   if (var == VAR_TN) {
@@ -960,7 +964,9 @@ int build_stages(cg_plan* p, const cg_desc* d) {
     auto get_vi = [&](int c, int r, int q) { return Vi[((size_t)c * n3 + r) * n3 + q]; };
     auto get_v = [&](int c, int r, int q) { return V[((size_t)c * n3 + r) * n3 + q]; };
     const bool chain = n3 <= kCfgs[kChainCfg].BN && !getenv("CURVIGPU_NO_CHAIN");
-    int r2 = chain ? add_stage(p, VAR_TN, EPI_CHAIN, n1 * n2, n3, n3, 1, BUF_X, BUF_Y, n3, get_vi, kChainCfg)
+    const char* ccfg = getenv("CURVIGPU_CHAIN_CFG");  // measurement knob
+    const int chain_cfg = (ccfg && atoi(ccfg) == kChainCfg16) ? kChainCfg16 : kChainCfg;
+    int r2 = chain ? add_stage(p, VAR_TN, EPI_CHAIN, n1 * n2, n3, n3, 1, BUF_X, BUF_Y, n3, get_vi, chain_cfg)
                    : add_stage(p, VAR_TN, EPI_PHI, n1 * n2, n3, n3, 1, BUF_X, BUF_Y, n3, get_vi);
     if (r2) return r2;
     Stage& s0 = p->stages.back();
@@ -972,7 +978,7 @@ int build_stages(cg_plan* p, const cg_desc* d) {
     if (chain) {
       double* op2 = nullptr;
       *cur = BUF_Y;
-      return upload_operator(p, VAR_TN, n3, get_v, &op2, &s0.opmap2, kCfgs[kChainCfg].BN);
+      return upload_operator(p, VAR_TN, n3, get_v, &op2, &s0.opmap2, kCfgs[chain_cfg].BN);
     }
     *cur = BUF_X;
     return add_stage(p, VAR_TN, EPI_STORE, n1 * n2, n3, n3, 1, BUF_Y, BUF_X, n3, get_v);

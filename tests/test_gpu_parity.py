@@ -433,7 +433,8 @@ def ensemble_plan_lanes(inputs, params, lanes):
 def test_ball_chained_polar_products_match_two_stages_bitwise(monkeypatch, theta_mode, dims):
     """The ball's two polar-mode products (x3 V^-1, o Phi_outer, x3 V) run as
     one chained kernel (intermediate in shared memory, zero column blocks
-    and k steps skipped) and, under CURVIGPU_NO_CHAIN, as two GEMM stages:
+    and k steps skipped; 32- and 16-row tiles) and, under CURVIGPU_NO_CHAIN,
+    as two GEMM stages:
     the plans differ by one stage and give bitwise-equal fields after 25
     steps (odd n3 = 7: padded rows; n3 = 128: the chain tile's full width);
     the chained run also matches the oracle."""
@@ -445,9 +446,10 @@ def test_ball_chained_polar_products_match_two_stages_bitwise(monkeypatch, theta
     kin = sysm.kinetics
     W0 = torch.from_numpy(np.stack([c.initial for c in sysm.components])[None]).cuda()
     outs, nstages = [], []
-    for chain in (True, False):
-        if chain:
+    for mode in ("14", "15", None):  # chain tile 32 x 128 (default), 16 x 128, two stages
+        if mode:
             monkeypatch.delenv("CURVIGPU_NO_CHAIN", raising=False)
+            monkeypatch.setenv("CURVIGPU_CHAIN_CFG", mode)
         else:
             monkeypatch.setenv("CURVIGPU_NO_CHAIN", "1")
         plan = SplitPlan(geos, 1, kin.kind, kin.param_vector()[None, :], theta=theta_mode)
@@ -456,8 +458,8 @@ def test_ball_chained_polar_products_match_two_stages_bitwise(monkeypatch, theta
         bad = torch.full((1, 2), INT32_MAX, dtype=torch.int32, device="cuda")
         plan.run(s, 0, 25, bad)
         outs.append(s.cpu().numpy())
-    assert nstages[0] == nstages[1] - 1
-    assert np.array_equal(outs[0], outs[1])
+    assert nstages[0] == nstages[1] == nstages[2] - 1
+    assert np.array_equal(outs[0], outs[2]) and np.array_equal(outs[1], outs[2])
     if dims != (100, 100, 100):
         osys = ocfg.BUILDERS[4](dims, initial=[c.initial for c in sysm.components])
         ref = orc.integrate(osys, 25, 25 * tau)
