@@ -262,9 +262,12 @@ class SplitPlan:
     ``(batch, ncomp, *grid)``, C-contiguous, reference axis order.
     """
 
-    # runs per lane below which a plan is not split into lanes (auto mode):
-    # each lane's kernels need several waves of work (profiles/r01_lanes.txt)
-    LANE_MIN_RUNS = 128
+    # runs per lane below which a plan is not split into lanes (auto mode).
+    # Measured at the per-rank shard sizes of the 1/2/4/8-GPU ensemble
+    # (profiles/r01_shard_sizes.jsonl): two lanes gain 1.5 % at 512 runs,
+    # 6 % at 128 and 14 % at 64 runs (the 8-GPU shard), where one plan's
+    # kernels run 1-2 ragged waves; 3 lanes add nothing (profiles/r01_lanes.txt)
+    LANE_MIN_RUNS = 32
 
     def __init__(self, geos, batch: int = 1, kinetics: str = "external",
                  kin_params=None, lifts=None, theta: str | None = None, ops_per_run: bool = False,

@@ -364,6 +364,7 @@ def test_fused_front_cta_variants_match_oracle_and_each_other(monkeypatch, theta
 
     for k, v in variant.items():
         monkeypatch.setenv(k, v)
+    monkeypatch.setenv("CURVIGPU_LANES", "1")  # one 160-run plan (two lanes would halve it)
     ens = pcfg.config5_inputs(100, 160)
     plan = _ensemble_plan(ens, 1e-3)
     state = torch.from_numpy(ens.states).cuda()
