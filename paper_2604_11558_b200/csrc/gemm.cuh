@@ -95,7 +95,7 @@ __device__ __forceinline__ int chain_xor(int r) { return (r & 1) | ((r & 2) << 1
 // rank order -- a fixed summation order, so results stay bitwise
 // reproducible -- then runs the epilogue alone.  Handshakes are mbarriers
 // armed across the cluster (red_full in rank 0, red_empty in each peer).
-template <int VAR, int BM, int BN, int WM, int WN, int STAGES, int EPI, int MINB, int KS = 1>
+template <int VAR, int BM, int BN, int WM, int WN, int STAGES, int EPI, int MINB, int KS = 1, bool RAG = false>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
     gemm_f64_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                     const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapO,
@@ -380,30 +380,54 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
           slice(std::integral_constant<int, NT>{});
         }
       } else {
+        // RAG (a separate instantiation for NN stages whose M or K is not a
+        // tile multiple, e.g. n = 100): skip what only adds zeros -- operator
+        // rows past M (the last m tile) and the k8 half-slice past K -- by
+        // warp-uniform branches to code with a compile-time count of live
+        // 8-row blocks ML (predicated-off DMMAs would still issue).  Keeping it
+        // out of the plain kernels keeps their code unchanged (measured: the
+        // extra paths in one kernel cost the aligned stages 4-8 %).
+        constexpr bool SKIP = RAG;
+        auto slice = [&](auto mlive, auto kskip) {
+          constexpr int ML = decltype(mlive)::value;
 #pragma unroll
-        for (int k8 = 0; k8 < 16; k8 += 8) {
+          for (int k8 = 0; k8 < 16; k8 += 8) {
+            if (decltype(kskip)::value && kt * 16 + k8 >= p.K) break;
 #pragma unroll
-          for (int sub = 0; sub < 2; ++sub) {
-            const int k = k8 + 2 * tq + sub;
-            const int kx = k & 7;
-            double a[MT], b[NT];
+            for (int sub = 0; sub < 2; ++sub) {
+              const int k = k8 + 2 * tq + sub;
+              const int kx = k & 7;
+              double a[ML > 0 ? ML : 1], b[NT];
 #pragma unroll
-            for (int i = 0; i < MT; ++i) {
-              const int m = wm0 + i * 8 + g;
-              const int mm = m & 15;
-              a[i] = sa[(m >> 4) * 256 + k * 16 + ((((mm >> 1) ^ kx)) << 1) + (mm & 1)];
+              for (int i = 0; i < ML; ++i) {
+                const int m = wm0 + i * 8 + g;
+                const int mm = m & 15;
+                a[i] = sa[(m >> 4) * 256 + k * 16 + ((((mm >> 1) ^ kx)) << 1) + (mm & 1)];
+              }
+#pragma unroll
+              for (int j = 0; j < NT; ++j) {
+                const int n = wn0 + j * 8 + g;
+                const int nn = n & 15;
+                b[j] = sb[(n >> 4) * 256 + k * 16 + ((((nn >> 1) ^ kx)) << 1) + (nn & 1)];
+              }
+#pragma unroll
+              for (int i = 0; i < ML; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
             }
-#pragma unroll
-            for (int j = 0; j < NT; ++j) {
-              const int n = wn0 + j * 8 + g;
-              const int nn = n & 15;
-              b[j] = sb[(n >> 4) * 256 + k * 16 + ((((nn >> 1) ^ kx)) << 1) + (nn & 1)];
-            }
-#pragma unroll
-            for (int i = 0; i < MT; ++i)
-#pragma unroll
-              for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
           }
+        };
+        using KS_ON = std::true_type;
+        using KS_OFF = std::false_type;
+        if constexpr (SKIP) {
+          static_assert(MT == 2, "ragged tiles: two 8-row blocks per warp");
+          const int ml = (p.M - m0 - wm0 + 7) >> 3;  // live 8-row blocks of this warp
+          if (ml >= 2)
+            slice(std::integral_constant<int, 2>{}, KS_ON{});
+          else if (ml == 1)
+            slice(std::integral_constant<int, 1>{}, KS_ON{});
+        } else {
+          slice(std::integral_constant<int, MT>{}, KS_OFF{});
         }
       }
       // Generic-proxy reads (the fragment LDS) of a stage followed by the

@@ -117,15 +117,16 @@ int make_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
 struct TileCfg {
   int BM, BN;
 };
-constexpr int kNumCfg = 16;
+constexpr int kNumCfg = 17;
 constexpr int kChainCfg = 14;  // EPI_CHAIN only: 32 rows x all (<= 128) columns, 8 warps of 16x32
 constexpr int kChainCfg16 = 15;  // EPI_CHAIN, 16-row tiles on 4 warps at 3 CTAs/SM (CURVIGPU_CHAIN_CFG=15)
+constexpr int kRaggedCfg = 16;   // cfg 12 for NN stages with M or K off the tile grid (zero-block skips)
 // 7, 8: the 64x64 configuration split-K over clusters of 2 / 4 CTAs
 // 9, 10: 64x64 tiles on 8 consumer warps (32x16 / 16x32 warp tiles); 11: 10 split-K over 2-CTA clusters
 // 12: 32x32 tiles on 4 warps of 16x16 (stages with very few 64x64 tiles); 13: 12 split-K over 2-CTA clusters
 constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {64, 128}, {128, 128}, {64, 64},
                                     {64, 64}, {64, 64}, {64, 64}, {64, 64}, {64, 64},
-                                    {32, 32}, {32, 32}, {32, 128}, {16, 128}};
+                                    {32, 32}, {32, 32}, {32, 128}, {16, 128}, {32, 32}};
 
 // BM, BN, warp tile, stages; 32x32 warp tiles keep the accumulators +
 // fragments under ~160 registers without spills.
@@ -146,10 +147,10 @@ constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {
 // configure_only: set the dynamic shared memory opt-in (done at plan
 // creation, never inside a stream capture).  KS > 1 launches clusters of KS
 // CTAs that split each tile's k range (gemm.cuh).
-template <int VAR, int BM, int BN, int WM, int WN, int ST, int MINB, int EPI, int KS = 1>
+template <int VAR, int BM, int BN, int WM, int WN, int ST, int MINB, int EPI, int KS = 1, bool RAG = false>
 int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mw, const CUtensorMap& mo,
                   const GemmParams& p, cudaStream_t stream, bool configure_only) {
-  auto kern = gemm_f64_kernel<VAR, BM, BN, WM, WN, ST, EPI, MINB, KS>;
+  auto kern = gemm_f64_kernel<VAR, BM, BN, WM, WN, ST, EPI, MINB, KS, RAG>;
   constexpr int smem = gemm_smem_bytes<BM, BN, ST>();
   constexpr int threads = (BM / WM) * (BN / WN) * 32 + 32;
   static int resident = 0;  // CTAs (KS = 1) or clusters (KS > 1) of this instantiation that fit at once
@@ -240,6 +241,7 @@ int launch_gemm_cfg(int cfg, const Maps& m, const GemmParams& p, cudaStream_t st
     case 11: return launch_gemm_t<VAR, CFG10, EPI, 2>(m.a, m.b, m.w, m.o, p, stream, conf);
     case 12: return launch_gemm_t<VAR, CFG12, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
     case 13: return launch_gemm_t<VAR, CFG12, EPI, 2>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case 16: return launch_gemm_t<VAR, CFG12, EPI, 1, VAR == VAR_NN>(m.a, m.b, m.w, m.o, p, stream, conf);
     default: return launch_gemm_t<VAR, CFG6, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
   }
 }
@@ -452,7 +454,6 @@ int pick_cfg(int var, long long nbatch, int M, int N, int K, int stage_index) {
   // reduction and cluster handshakes; the split-K configurations 7, 8, 11, 13
   // stay selectable through CURVIGPU_TILE_CFG for measurement and are tested,
   // but the 32x32 tiles below now beat them).
-  (void)var;
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -468,7 +469,10 @@ int pick_cfg(int var, long long nbatch, int M, int N, int K, int stage_index) {
   // 64x64 (config 5: 277 vs 309 us) (profiles/r01_warp8_sweep.txt).
   (void)K;
   const long long tiles = nbatch * ((M + 63) / 64) * ((N + 63) / 64);
-  return tiles <= 8LL * sms ? 12 : 10;
+  if (tiles > 8LL * sms) return 10;
+  // NN stages with M or K off the 32 x 16 grid (n = 100) take the
+  // zero-block-skipping instantiation: ball rho stage 23.2 -> 21.4 us
+  return (var == VAR_NN && (M % 32 != 0 || K % 16 != 0)) ? kRaggedCfg : 12;
 }
 
 // Build one GEMM stage: operator L (n x n) via `get`, shapes, epilogue.
