@@ -290,7 +290,8 @@ int launch_fbuild_t(const StencilParams& p, cudaStream_t s, bool configure_only)
   if (nl > 512) return fail(CG_EUNSUPPORTED, "contiguous axis longer than 512");
   const size_t smem = (size_t)(KIN == KIN_EXTERNAL ? 1 : 2) * S::ROWS * nl * sizeof(double);
   if (smem > 200 * 1024) return fail(CG_EUNSUPPORTED, "F-build tile exceeds shared memory");
-  const dim3 grid((unsigned)((p.n1 + S::RB - 1) / S::RB), S::D3 ? (unsigned)p.n2 : 1u, (unsigned)p.batch);
+  const dim3 grid((unsigned)((p.n1 + S::RB - 1) / S::RB), S::D3 ? (unsigned)((p.n2 + S::JB - 1) / S::JB) : 1u,
+                  (unsigned)p.batch);
   const unsigned threads = (unsigned)((nl + 31) / 32 * 32);
   int rc = launch_pdl(fbuild_rows_kernel<GEOM, KIN>, grid, dim3(threads), smem, s, p);
   if (rc) return rc;

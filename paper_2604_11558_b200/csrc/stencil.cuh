@@ -126,11 +126,22 @@ struct FbuildShape {
 #ifndef CG_RB3
 #define CG_RB3 4
 #endif
+#ifndef CG_JB3
+#define CG_JB3 2
+#endif
   static constexpr int RB = D3 ? CG_RB3 : 8;         // interior rows per CTA
-  static constexpr int ROWS = D3 ? 3 * RB + 2 : RB + 2;  // staged rows per component
+  // 3-D: JB consecutive theta columns per CTA share their theta neighbours:
+  // staged rows = JB (RB + 2) centre rows + 2 RB theta-halo rows.  JB = 2
+  // (2.5 staged rows per output row instead of 3.5): cylinder F-build
+  // 11.8 -> 10.9 us, ball 14.6 -> 13.8 us; JB = 4 (2.0, but a quarter of the
+  // CTAs: ragged waves) measured 14.8 / 14.7 us
+  static constexpr int JB = D3 ? CG_JB3 : 1;
+  static constexpr int ROWS = D3 ? JB * (RB + 2) + 2 * RB : RB + 2;  // staged rows per component
 };
 
 // stage component X's rows for this CTA into s[ROWS][nl]
+// 3-D: X points at column j0; centre block jj at rows jj (RB + 2) ..., the
+// theta halo (columns j0 - 1 and j0 + jn, periodic) at JB (RB + 2) + [0, 2 RB)
 template <int GEOM>
 __device__ __forceinline__ void stage_rows(double* s, const double* __restrict__ X, int i0, int j, int n1, int n2,
                                            int nl, long long rs, int jst) {
@@ -138,21 +149,27 @@ __device__ __forceinline__ void stage_rows(double* s, const double* __restrict__
   const bool periodic_walk = (GEOM == 1);
   const int l = threadIdx.x;
   if (l >= nl) return;
+  const int jn = S::D3 ? min(S::JB, n2 - j) : 1;  // valid columns of this CTA
 #pragma unroll
-  for (int r = 0; r < S::RB + 2; ++r) {
-    int i = i0 - 1 + r;
-    if (i < 0) i = periodic_walk ? n1 - 1 : 0;
-    if (i >= n1) i = periodic_walk ? i - n1 : n1 - 1;
-    s[r * nl + l] = __ldg(X + (long long)i * rs + l);
+  for (int jj = 0; jj < S::JB; ++jj) {
+    const long long jo = (long long)(jj < jn ? jj : jn - 1) * jst;
+#pragma unroll
+    for (int r = 0; r < S::RB + 2; ++r) {
+      int i = i0 - 1 + r;
+      if (i < 0) i = periodic_walk ? n1 - 1 : 0;
+      if (i >= n1) i = periodic_walk ? i - n1 : n1 - 1;
+      s[(jj * (S::RB + 2) + r) * nl + l] = __ldg(X + (long long)i * rs + jo + l);
+    }
   }
   if (S::D3) {
     const int jm = (j == 0) ? n2 - 1 : j - 1;
-    const int jp = (j == n2 - 1) ? 0 : j + 1;
+    const int jp = (j + jn == n2) ? 0 : j + jn;
+    constexpr int H = S::JB * (S::RB + 2);
 #pragma unroll
     for (int r = 0; r < S::RB; ++r) {
       const int i = min(i0 + r, n1 - 1);
-      s[(S::RB + 2 + r) * nl + l] = __ldg(X + (long long)i * rs + (long long)(jm - j) * jst + l);
-      s[(2 * S::RB + 2 + r) * nl + l] = __ldg(X + (long long)i * rs + (long long)(jp - j) * jst + l);
+      s[(H + r) * nl + l] = __ldg(X + (long long)i * rs + (long long)(jm - j) * jst + l);
+      s[(H + S::RB + r) * nl + l] = __ldg(X + (long long)i * rs + (long long)(jp - j) * jst + l);
     }
   }
 }
@@ -191,10 +208,13 @@ __device__ __forceinline__ CompCoef comp_coef(const StencilParams& p, int c, int
 
 // coeff-free diffusion action at interior row r (global row i), column l,
 // from the shared-memory stage s (rows r, r+1, r+2 = i-1, i, i+1)
+// (3-D: theta column jj of the CTA's jn; its theta neighbours are the adjacent
+// centre blocks or the halo rows)
 template <int GEOM>
-__device__ __forceinline__ double diffusion_rows(const CompCoef& k, const RowCoef& rc, const double* s, int r, int l,
-                                                 int nl) {
+__device__ __forceinline__ double diffusion_rows(const CompCoef& k, const RowCoef& rc, const double* s0, int r, int l,
+                                                 int nl, int jj = 0, int jn = 1) {
   using S = FbuildShape<GEOM>;
+  const double* s = s0 + jj * (S::RB + 2) * nl;
   const double xm = s[r * nl + l], x0 = s[(r + 1) * nl + l], xp = s[(r + 2) * nl + l];
   int ll = l - 1, lr = l + 1;
   if (GEOM == 0) {  // periodic contiguous axis
@@ -215,7 +235,9 @@ __device__ __forceinline__ double diffusion_rows(const CompCoef& k, const RowCoe
     const double rr = k.la * x0 + k.lc * xl + k.lb * xr;
     return q * k.ld + rr;
   } else {
-    const double ym = s[(S::RB + 2 + r) * nl + l], yp = s[(2 * S::RB + 2 + r) * nl + l];
+    constexpr int H = S::JB * (S::RB + 2);
+    const double ym = jj > 0 ? s0[((jj - 1) * (S::RB + 2) + r + 1) * nl + l] : s0[(H + r) * nl + l];
+    const double yp = jj + 1 < jn ? s0[((jj + 1) * (S::RB + 2) + r + 1) * nl + l] : s0[(H + S::RB + r) * nl + l];
     const double rr = rc.a * x0 + rc.c * xm + rc.b * xp;
     const double q = k.th_off * ym + k.th_diag * x0 + k.th_off * yp;
     const double dr = rc.d;
@@ -257,7 +279,8 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
   const int l = threadIdx.x;
   const int lcl = l < nl ? l : nl - 1;
   const int i0 = blockIdx.x * S::RB;
-  const int j = S::D3 ? (int)blockIdx.y : 0;
+  const int j = S::D3 ? (int)blockIdx.y * S::JB : 0;  // first theta column
+  const int jn = S::D3 ? min(S::JB, p.n2 - j) : 1;
   const int b = blockIdx.z;
   const long long rsw = S::D3 ? (long long)p.n2 * p.ldw : (long long)p.ldw;
   const long long rsf = S::D3 ? (long long)p.n2 * p.ldf : (long long)p.ldf;
@@ -276,15 +299,18 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
       __syncthreads();
       if (l < nl) {
         const CompCoef k = comp_coef<GEOM>(p, ob + c, l, nl);
+        for (int jj = 0; jj < jn; ++jj) {
 #pragma unroll
-        for (int r = 0; r < S::RB; ++r) {
-          const int i = i0 + r;
-          if (i >= n1) break;
-          const long long idx = fbase + (long long)c * p.npf + (long long)i * rsf + l;
-          double val = 0.0;
-          if (p.with_diffusion) val = k.coeff * diffusion_rows<GEOM>(k, rcs[(c < 8 ? c : 7) * S::RB + r], fb_smem, r, l, nl);
-          if (p.with_reaction) val = p.with_diffusion ? __dadd_rn(val, __ldg(p.G + idx)) : __ldg(p.G + idx);
-          p.F[idx] = val;
+          for (int r = 0; r < S::RB; ++r) {
+            const int i = i0 + r;
+            if (i >= n1) break;
+            const long long idx = fbase + (long long)jj * p.ldf + (long long)c * p.npf + (long long)i * rsf + l;
+            double val = 0.0;
+            if (p.with_diffusion)
+              val = k.coeff * diffusion_rows<GEOM>(k, rcs[(c < 8 ? c : 7) * S::RB + r], fb_smem, r, l, nl, jj, jn);
+            if (p.with_reaction) val = p.with_diffusion ? __dadd_rn(val, __ldg(p.G + idx)) : __ldg(p.G + idx);
+            p.F[idx] = val;
+          }
         }
       }
     }
@@ -306,27 +332,30 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
     __syncthreads();
     if (l >= nl) return;
     double* __restrict__ Fo = p.F;
+    for (int jj = 0; jj < jn; ++jj) {
 #pragma unroll
     for (int r = 0; r < S::RB; ++r) {
       const int i = i0 + r;
       if (i >= n1) break;
-      const long long off = fbase + (long long)i * rsf + l;
+      const long long off = fbase + (long long)jj * p.ldf + (long long)i * rsf + l;
+      const int cs = (jj * (S::RB + 2) + r + 1) * nl + l;  // centre value in the stage
       double g0 = 0.0, g1 = 0.0;
       if (with_r) {
-        double u = fb_smem[(r + 1) * nl + l], v = fb_smem[plane + (r + 1) * nl + l];
+        double u = fb_smem[cs], v = fb_smem[plane + cs];
         if (lift0 != 0.0) u = __dadd_rn(u, lift0);
         if (lift1 != 0.0) v = __dadd_rn(v, lift1);
         reaction<KIN>(kin, u, v, g0, g1);
       }
       double fu = g0, fv = g1;
       if (with_d) {
-        const double du = k0.coeff * diffusion_rows<GEOM>(k0, rcs[r], fb_smem, r, l, nl);
-        const double dv = k1.coeff * diffusion_rows<GEOM>(k1, rcs[S::RB + r], fb_smem + plane, r, l, nl);
+        const double du = k0.coeff * diffusion_rows<GEOM>(k0, rcs[r], fb_smem, r, l, nl, jj, jn);
+        const double dv = k1.coeff * diffusion_rows<GEOM>(k1, rcs[S::RB + r], fb_smem + plane, r, l, nl, jj, jn);
         fu = with_r ? __dadd_rn(du, g0) : du;
         fv = with_r ? __dadd_rn(dv, g1) : dv;
       }
       Fo[off] = fu;
       Fo[off + p.npf] = fv;
+    }
     }
   }
 }
