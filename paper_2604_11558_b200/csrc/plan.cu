@@ -117,16 +117,17 @@ int make_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
 struct TileCfg {
   int BM, BN;
 };
-constexpr int kNumCfg = 17;
+constexpr int kNumCfg = 18;
 constexpr int kChainCfg = 14;  // EPI_CHAIN only: 32 rows x all (<= 128) columns, 8 warps of 16x32
 constexpr int kChainCfg16 = 15;  // EPI_CHAIN, 16-row tiles on 4 warps at 3 CTAs/SM (CURVIGPU_CHAIN_CFG=15)
 constexpr int kRaggedCfg = 16;   // cfg 12 for NN stages with M or K off the tile grid (zero-block skips)
+constexpr int kWideCfg = 17;     // 16 x 128 tiles (4 warps of 16x32, 3 CTAs/SM) for TN stages with N = 128
 // 7, 8: the 64x64 configuration split-K over clusters of 2 / 4 CTAs
 // 9, 10: 64x64 tiles on 8 consumer warps (32x16 / 16x32 warp tiles); 11: 10 split-K over 2-CTA clusters
 // 12: 32x32 tiles on 4 warps of 16x16 (stages with very few 64x64 tiles); 13: 12 split-K over 2-CTA clusters
 constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {64, 128}, {128, 128}, {64, 64},
                                     {64, 64}, {64, 64}, {64, 64}, {64, 64}, {64, 64},
-                                    {32, 32}, {32, 32}, {32, 128}, {16, 128}, {32, 32}};
+                                    {32, 32}, {32, 32}, {32, 128}, {16, 128}, {32, 32}, {16, 128}};
 
 // BM, BN, warp tile, stages; 32x32 warp tiles keep the accumulators +
 // fragments under ~160 registers without spills.
@@ -242,6 +243,7 @@ int launch_gemm_cfg(int cfg, const Maps& m, const GemmParams& p, cudaStream_t st
     case 12: return launch_gemm_t<VAR, CFG12, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
     case 13: return launch_gemm_t<VAR, CFG12, EPI, 2>(m.a, m.b, m.w, m.o, p, stream, conf);
     case 16: return launch_gemm_t<VAR, CFG12, EPI, 1, VAR == VAR_NN>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case 17: return launch_gemm_t<VAR, CFG15, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
     default: return launch_gemm_t<VAR, CFG6, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
   }
 }
@@ -439,7 +441,7 @@ int pick_cfg(int var, long long nbatch, int M, int N, int K, int stage_index) {
       if (*q == ',') ++q;
     }
     const int v = nv == 1 ? vals[0] : (stage_index < nv ? vals[stage_index] : -1);
-    if (v >= 0 && v < kChainCfg) return v;
+    if ((v >= 0 && v < kChainCfg) || v == 17) return v;
   }
   // Measured on B200 with the TMA epilogue (tools/sweep_tiles.py,
   // profiles/r01_tile_sweep_tmaepi.txt): 64x64 tiles, 4-stage ring, 2 CTAs/SM
@@ -471,6 +473,11 @@ int pick_cfg(int var, long long nbatch, int M, int N, int K, int stage_index) {
   (void)K;
   const long long tiles = nbatch * ((M + 63) / 64) * ((N + 63) / 64);
   if (tiles > 8LL * sms) return 10;
+  // TN stages exactly 128 wide with many rows (the cylinder's phi1_z stage):
+  // 16 x 128 tiles, 6 operand rows per 8 DMMAs instead of 4 per 4, 1024
+  // tiles in balanced rounds: 21.6 -> 21.1 us.  (NN stages and the sphere's
+  // 256-wide stage measured slower with it.)
+  if (var == VAR_TN && N == 128 && K % 16 == 0 && M % 16 == 0 && nbatch * (M / 16) >= 2LL * sms) return kWideCfg;
   // NN stages with M or K off the 32 x 16 grid (n = 100) take the
   // zero-block-skipping instantiation: ball rho stage 23.2 -> 21.4 us
   return (var == VAR_NN && (M % 32 != 0 || K % 16 != 0)) ? kRaggedCfg : 12;
