@@ -117,6 +117,33 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_ranks(args):
+    """`bench.py --gpus N` started without a launcher: re-exec under torchrun
+    with N local ranks (one process per GPU).  Refuses loudly when the box has
+    fewer than N GPUs instead of silently timing one rank."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible CUDA devices, found {have}",
+              file=sys.stderr, flush=True)
+        sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def dist_setup(args):
     import torch
     import torch.distributed as dist
@@ -124,6 +151,10 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} rank(s)")
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {rank} wants cuda:{local}, only {torch.cuda.device_count()} device(s)")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -137,6 +168,19 @@ def barrier(world):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+
+
+def per_rank(values, world):
+    """Every rank's list of floats, on every rank (rank order)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(values, dtype=torch.float64, device="cuda")
+    if world == 1:
+        return [t.tolist()]
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [o.tolist() for o in out]
 
 
 def max_over_ranks(value, world):
@@ -306,26 +350,41 @@ def bulk_surface_gpu(key, steps=320, warmup=32):
 
 
 def bulk_surface_cpu(key, steps=3):
-    """The same step through the oracle port on the host (BLAS threads as set)."""
+    """The same coupled step on the host: the real reference (baseline/_ref)
+    through its own run_simulation when installed, else the oracle port."""
     import time
 
+    from oracle import ref_bench
+
+    name, dims, m, t_star = BULK_SURFACE[key]
+    tau = t_star / m
+    threads = os.environ.get("OPENBLAS_NUM_THREADS", "default (all cores)")
+    if ref_bench.available():
+        from oracle import ref_configs
+
+        ref_configs.load_curvipat()
+        from curvipat import models as ref_models
+
+        system = ref_models.build_system(name, dims, 1)
+        sec = ref_bench.timed_run(system, 1, steps, tau) / steps
+        dof = sum(int(c.initial.size) for c in system.components)
+        return {"model": name, "ms_per_step": sec * 1e3, "dof_steps_per_s": dof / sec, "kind": "reference",
+                "threads": threads}
     from oracle import configs as ocfg
     from oracle import curvi_oracle as orc
     from paper_2604_11558_b200 import models
 
-    name, dims, m, t_star = BULK_SURFACE[key]
     system = models.build_system(name, dims, 1)
     init = [c.initial for c in system.components]
     d = tuple(dims.values())
     osys = ocfg.bs_ball(d, initial=init) if key.startswith("ball") else ocfg.bs_cylinder(d, initial=init)
-    tau = t_star / m
     orc.integrate(osys, 1, tau)
     t0 = time.perf_counter()
     orc.integrate(osys, steps, steps * tau)
     sec = (time.perf_counter() - t0) / steps
     dof = sum(int(c.initial.size) for c in system.components)
     return {"model": name, "ms_per_step": sec * 1e3, "dof_steps_per_s": dof / sec, "kind": "port",
-            "threads": os.environ.get("OPENBLAS_NUM_THREADS", "default (all cores)")}
+            "threads": threads}
 
 
 def engine_arm(args):
@@ -382,7 +441,10 @@ def engine_arm(args):
         ens.advance(chunk, from_host=True, to_host=True)
     e1.record(stream)
     barrier(world)
-    e2e_sec = max_over_ranks(e0.elapsed_time(e1) / 1e3, world)
+    e2e_local = e0.elapsed_time(e1) / 1e3
+    e2e_sec = max_over_ranks(e2e_local, world)
+    dev_local = sum(a.elapsed_time(b) for a, b in events) / 1e3
+    ranks = per_rank([float(lo), float(hi), dev_local, e2e_local], world)
 
     # the ensemble's one collective: final physical fields to rank 0
     t0 = time.perf_counter()
@@ -449,6 +511,9 @@ def engine_arm(args):
                 "api": "paper_2604_11558_b200.ensemble.Ensemble.advance (pinned host in/out)"},
         "gpu_launches": launches_per_step * args.steps,
         "gather_ms": gather_ms,
+        "per_rank": [{"rank": r, "runs": [int(v[0]), int(v[1])], "device_s": v[2], "e2e_s": v[3],
+                      "value": (v[1] - v[0]) * NCOMP * DIMS[0] * DIMS[1] * chunk * args.steps / v[2]}
+                     for r, v in enumerate(ranks)],
         "diverged_runs": int((bad.min(axis=1) < 2**31 - 1).sum()),
         "finite": finite,
     }
@@ -478,33 +543,81 @@ def host_cores():
         return os.cpu_count() or 1
 
 
-def cpu_baseline_ensemble(sample_steps=200, workers=None):
+def _cpu_pool(P):
+    """P host workers, one config-5 member each: the real reference from
+    baseline/_ref when installed (kind "reference"), else the oracle port."""
+    from oracle import ref_bench
+
+    if ref_bench.available():
+        return ref_bench.RefEnsemble(P, DIMS, RUNS), "reference"
     from oracle.cpu_bench import CpuEnsemble
 
+    return CpuEnsemble(P, DIMS, RUNS), "port"
+
+
+def _host_facts():
+    from oracle import ref_bench
+
+    return {"cpu_model": ref_bench.cpu_model(), "host_cores": host_cores()}
+
+
+def cpu_baseline_ensemble(sample_steps=200, workers=None):
+    """SURVEY 8(d) steps 1-3 on the GPU box's host: all cores (one process
+    per core x 1 BLAS thread, one member each) and the P = 1 leg, the CPU
+    model, the BLAS build, and setup (build_system + IC, prepare) reported
+    apart from stepping."""
     P = workers or host_cores()
-    pool = CpuEnsemble(P, DIMS, RUNS)
+    pool, kind = _cpu_pool(P)
     try:
         sec = pool.sample(sample_steps)
+        setup = getattr(pool, "setup", None)
+        blas = getattr(pool, "blas", None)
     finally:
         pool.close()
+    one, _ = _cpu_pool(1)
+    try:
+        sec1 = one.sample(sample_steps)
+    finally:
+        one.close()
     dof = NCOMP * DIMS[0] * DIMS[1]
-    return {"value": P * dof * sample_steps / sec, "unit": UNIT, "cores": P, "kind": "port",
+    what = ("curvipat.integrators.run_simulation from baseline/_ref (the unmodified reference), stepping timed "
+            "by its own sample_hook" if kind == "reference" else
+            "oracle/ NumPy restatement of curvipat's split EE step (baseline/_ref not installed)")
+    return {"value": P * dof * sample_steps / sec, "unit": UNIT, "cores": P, "kind": kind,
             "sample": f"{P} ensemble members x {sample_steps} steps, one process per core, 1 BLAS thread each "
-                      f"(oracle/ NumPy restatement of curvipat's split EE step; {sec:.2f} s wall)"}
+                      f"({what}; {sec:.2f} s wall)",
+            "p1": {"value": dof * sample_steps / sec1, "cores": 1, "ms_per_step": sec1 / sample_steps * 1e3},
+            "setup_s": setup, "blas": blas, **_host_facts()}
 
 
 def cpu_per_config():
-    from oracle.cpu_bench import time_config
+    """Configs 1-4 on the host at 1 BLAS thread and at all cores (one
+    process), through the real reference when installed."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import ref_bench
 
     out = []
     for k, steps in ((1, 100), (2, 10), (3, 3), (4, 3)):
-        sec = time_config(k, steps)
         dims = {1: (64, 128), 2: (512, 256), 3: (64, 128, 128), 4: (100, 100, 100)}[k]
         dof = 2
         for d in dims:
             dof *= d
-        out.append({"config": k, "ms_per_step": sec * 1e3, "dof_steps_per_s": dof / sec,
-                    "threads": os.environ.get("OPENBLAS_NUM_THREADS", "default (all cores)")})
+        row = {"config": k}
+        for label, limit in (("p1", 1), ("pall", None)):
+            with threadpool_limits(limits=limit):
+                if ref_bench.available():
+                    r = ref_bench.time_config(k, steps)
+                    sec, kind = r["sec_per_step"], "reference"
+                    row["setup_s"] = {"build_system_ic_s": r["build_system_ic_s"], "prepare_s": r["prepare_s"]}
+                else:
+                    from oracle.cpu_bench import time_config
+
+                    sec, kind = time_config(k, steps), "port"
+            row[label] = {"ms_per_step": sec * 1e3, "dof_steps_per_s": dof / sec,
+                          "threads": 1 if limit == 1 else host_cores()}
+            row["kind"] = kind
+        out.append(row)
     return out
 
 
@@ -513,24 +626,25 @@ def reference_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    from oracle.cpu_bench import CpuEnsemble
-
     P = host_cores()
     per_step = 20  # time steps each member advances per bench step (bounded sample)
-    pool = CpuEnsemble(P, DIMS, RUNS)
+    pool, kind = _cpu_pool(P)
     try:
         for _ in range(args.warmup):
             pool.sample(per_step)
         total = 0.0
         for _ in range(args.steps):
             total += pool.sample(per_step)
+        setup = getattr(pool, "setup", None)
     finally:
         pool.close()
     dof = NCOMP * DIMS[0] * DIMS[1]
     value = P * dof * per_step * args.steps / total
+    what = ("the unmodified reference curvipat (baseline/_ref) through curvipat.integrators.run_simulation, "
+            "stepping timed by its own sample_hook" if kind == "reference" else
+            "oracle/ NumPy port of curvipat's split EE (baseline/_ref not installed)")
     sample = (f"{P} of the 512 ensemble members x {per_step} time steps per bench step, one process per core "
-              f"x 1 BLAS thread (oracle/ NumPy port of curvipat's split EE; the Python reference cannot "
-              f"travel to the GPU box)")
+              f"x 1 BLAS thread ({what})")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
@@ -538,7 +652,8 @@ def reference_arm(args):
         "data": "synthetic: reference-seeded xoshiro256++ initial fields",
         "config": {"workload": "BASELINE config 5 ensemble (512 x anomalous disk 128x256), bounded CPU sample",
                    "runs_sampled": P, "time_steps_per_bench_step": per_step},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": kind, "sample": sample,
+                         "setup_s": setup, **_host_facts()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -546,6 +661,10 @@ def reference_arm(args):
 
 def main():
     args = parse()
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if args.impl == "engine" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        launch_ranks(args)
     if args.impl == "reference":
         reference_arm(args)
     else:

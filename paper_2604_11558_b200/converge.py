@@ -17,7 +17,8 @@ import math
 import numpy as np
 
 from .integrators import INT32_MAX, DivergenceError, SplitPlan, engine_kinetics, prepare
-from .models import build_system
+from .coupled import CoupledPlan
+from .models import BulkSurfaceCoupling, build_system
 
 
 def relative_error(states: dict, reference: dict) -> float:
@@ -52,6 +53,9 @@ def convergence_study(spec, dims: dict, t_star: float, m_list, *, m_ref: int | N
 
     system = build_system(spec, dims, seed)
     kin = engine_kinetics(system)
+    if isinstance(kin, BulkSurfaceCoupling):
+        fields = _coupled_runs(system, kin, t_star, [m_ref] + m_list)
+        return _table(m_list, fields)
     comps = list(system.components)
     names = [c.name for c in comps]
     lifts = [float(getattr(c, "lift", 0.0)) for c in comps]
@@ -78,7 +82,40 @@ def convergence_study(spec, dims: dict, t_star: float, m_list, *, m_ref: int | N
         host = state[0].cpu().numpy()
         fields.append({n: host[i].copy() for i, n in enumerate(names)})
         plan.close()
+    return _table(m_list, fields)
+
+
+def _table(m_list, fields) -> dict:
+    """cmd_converge's table and slope from the m_ref run (fields[0]) and the
+    m_list runs (cli.py:286-312)."""
     reference = fields[0]
     table = [{"m": m, "err_split": relative_error(f, reference)} for m, f in zip(m_list, fields[1:])]
     slope = float(np.polyfit(np.log([e["m"] for e in table]), np.log([e["err_split"] for e in table]), 1)[0])
     return {"table": table, "slope": slope}
+
+
+def _coupled_runs(system, coupling, t_star: float, ms) -> list:
+    """The bulk-surface models (ball + sphere, cylinder + disk): one
+    CoupledPlan per m, each on its own stream so the runs overlap; lifted
+    fields per run, DivergenceError as run_simulation raises it."""
+    import torch
+
+    comps = list(system.components)
+    names = [c.name for c in comps]
+    lifts = [float(getattr(c, "lift", 0.0)) for c in comps]
+    runs = []
+    for m in ms:
+        tau = t_star / m
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            plan = CoupledPlan([prepare(c.ops, tau) for c in comps], coupling, lifts=lifts)
+            plan.load([c.initial for c in comps])
+            plan.run(0, m)
+        runs.append((m, plan, stream))
+    fields = []
+    for m, plan, stream in runs:
+        stream.synchronize()
+        plan.check_divergence(names)
+        fields.append({n: f.cpu().numpy().copy() for n, f in zip(names, plan.fields())})
+        plan.close()
+    return fields

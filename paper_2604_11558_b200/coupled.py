@@ -126,14 +126,16 @@ class CoupledPlan:
 
 
 def run_coupled(system, m: int, t_star: float, *, record_every=None, diagnostics=None, sample_hook=None,
-                as_torch: bool = False):
-    """run_simulation for a bulk-surface system (integrators.py:370-430)."""
-    from .integrators import RunResult
+                as_torch: bool = False, coupling=None):
+    """run_simulation for a bulk-surface system (integrators.py:370-430);
+    ``coupling`` is its BulkSurfaceCoupling (default: engine_kinetics)."""
+    from .integrators import RunResult, engine_kinetics
 
     tau = t_star / m
     comps = list(system.components)
     names = [c.name for c in comps]
-    plan = CoupledPlan([prepare(c.ops, tau) for c in comps], system.kinetics,
+    coupling = coupling if coupling is not None else engine_kinetics(system)
+    plan = CoupledPlan([prepare(c.ops, tau) for c in comps], coupling,
                        lifts=[float(getattr(c, "lift", 0.0)) for c in comps])
     plan.load([c.initial for c in comps])
     every = record_every or m

@@ -17,6 +17,8 @@
 
 #include <cuda_runtime.h>
 
+#include "common.cuh"
+
 namespace cg {
 
 enum { BS_BALL = 1, BS_CYLINDER = 2 };
@@ -68,7 +70,7 @@ __device__ __forceinline__ void cyl_flux(const CouplingParams& p, double ub, dou
                                           __dadd_rn(__dsub_rn(1.0, e3), __dmul_rn(e3, z5))),
                                 __dmul_rn(z5, __dadd_rn(1.0, __dmul_rn(e3, z5))));
   const double one_s = __dsub_rn(1.0, s);
-  pr = __dsub_rn(__dsub_rn(__dmul_rn(__dmul_rn(__dmul_rn(z2, ub), one_s), r), __dmul_rn(z3, __dmul_rn(__dmul_rn(r, r), r))),
+  pr = __dsub_rn(__dsub_rn(__dmul_rn(__dmul_rn(__dmul_rn(z2, ub), one_s), r), __dmul_rn(z3, cube_rn(r))),
                  __dmul_rn(z4, __dsub_rn(s, z5)));
   const double q1 = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(e1, vb), __dadd_rn(1.0, __dmul_rn(e2, r))), one_s),
                               __dsub_rn(1.0, __dmul_rn(e3, one_s)));

@@ -396,6 +396,29 @@ int dev_alloc(cg_plan* p, size_t bytes, void** out) {
   return CG_OK;
 }
 
+// X, Y, S2 (and S0 for padded storage), each the state's size: allocated by
+// the first entry point that touches them.  Not capture-safe by design: the
+// first call on a plan must not be made inside a caller's stream capture.
+int ensure_workspace(cg_plan* p) {
+  if (p->X) return CG_OK;
+  const size_t bytes = (size_t)p->elems * sizeof(double);
+  int rc;
+  double *X = nullptr, *Y = nullptr, *S2 = nullptr, *S0 = nullptr;
+  if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&X)))) return rc;
+  if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&Y)))) return rc;
+  if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&S2)))) return rc;
+  if (p->padded) {
+    if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&S0)))) return rc;
+    for (double* buf : {X, Y, S2, S0}) CUDA_TRY(cudaMemset(buf, 0, bytes));
+    CUDA_TRY(cudaDeviceSynchronize());
+  }
+  p->Y = Y;
+  p->S2 = S2;
+  p->S0 = S0;
+  p->X = X;
+  return CG_OK;
+}
+
 int upload(cg_plan* p, const double* host, size_t count, double** out) {
   if (!host) {
     *out = nullptr;
@@ -1266,17 +1289,9 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
 #undef OPT_IN
 #undef OPT_IN_R
   }
-  const size_t bytes = (size_t)p->elems * sizeof(double);
-  if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&p->X)))) return bail(rc);
-  if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&p->Y)))) return bail(rc);
-  if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&p->S2)))) return bail(rc);
-  if (p->padded) {
-    if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&p->S0)))) return bail(rc);
-    for (double* buf : {p->X, p->Y, p->S2, p->S0}) {
-      cudaError_t e0 = cudaMemset(buf, 0, bytes);
-      if (e0 != cudaSuccess) return bail(fail(CG_ECUDA, cudaGetErrorString(e0)));
-    }
-  }
+  // the state-sized workspaces (X, Y, S2, S0) are allocated on first use
+  // (ensure_workspace): a plan used only as a descriptor -- the parent of a
+  // laned SplitPlan, whose lanes step their own sub-plans -- never holds them
   if ((rc = dev_alloc(p, sizeof(int), reinterpret_cast<void**>(&p->step_dev)))) return bail(rc);
   if ((rc = dev_alloc(p, sizeof(int) * (size_t)p->B * C, reinterpret_cast<void**>(&p->scratch_bad))))
     return bail(rc);
@@ -1294,6 +1309,8 @@ int cg_plan_stage_count(const cg_plan* p) { return p ? (int)p->stages.size() : 0
 
 int cg_plan_copy_workspace(cg_plan* p, int which, double* dst, void* stream) {
   if (!p || !dst || which < 0 || which > 2) return fail(CG_EINVAL, "bad workspace request");
+  int rc = ensure_workspace(p);
+  if (rc) return rc;
   const double* src = which == 0 ? p->X : which == 1 ? p->Y : p->S2;
   if (p->padded) return repack(p, src, p->ld, dst, p->nl, static_cast<cudaStream_t>(stream));
   CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)p->elems * sizeof(double), cudaMemcpyDeviceToDevice,
@@ -1338,6 +1355,7 @@ int cg_run_stage(cg_plan* p, int stage, const double* W, double* W_out, int* fir
   if (stage < -2 || stage >= (int)p->stages.size()) return fail(CG_EINVAL, "bad stage index");
   if (stage == -2 && !p->fused_front) return fail(CG_EINVAL, "plan has no fused front kernel");
   if (p->padded) return fail(CG_EUNSUPPORTED, "per-stage access needs an even contiguous axis");
+  if (int rc = ensure_workspace(p)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (stage == -2) return launch_fused_front(p, W, false, s);
   if (stage < 0) return launch_fstage(p, W, nullptr, p->kin != CG_KIN_EXTERNAL, false, s);
@@ -1403,6 +1421,7 @@ int cg_step(cg_plan* p, const double* W, const double* G, double* W_out, void* s
 int cg_step_guarded(cg_plan* p, const double* W, const double* G, double* W_out, int* first_bad, void* stream) {
   if (!p || !W || !G || !W_out || !first_bad) return fail(CG_EINVAL, "null argument");
   if (W == W_out) return fail(CG_EINVAL, "W_out must not alias W");
+  if (int rc = ensure_workspace(p)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool count = first_bad != p->scratch_bad;
   if (!p->padded) return launch_step(p, W, W_out, G, false, first_bad, count, s);
@@ -1588,6 +1607,8 @@ int cg_coupled_run(cg_coupling* c, cg_plan* bulk, cg_plan* surf, double* Wb, dou
   if (bulk->geom != want || surf->geom != want_s) return fail(CG_EINVAL, "plan geometries do not match the coupling");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (nsteps == 0) return CG_OK;
+  if (int rc = ensure_workspace(bulk)) return rc;
+  if (int rc = ensure_workspace(surf)) return rc;
   // padded plans step their storage copies (S0) of the caller's fields
   double* wb = bulk->padded ? bulk->S0 : Wb;
   double* ws = surf->padded ? surf->S0 : Ws;
@@ -1726,6 +1747,7 @@ int cg_run(cg_plan* p, double* state, long long step0, long long nsteps, int* fi
   if (step0 < 0 || step0 + nsteps > INT_MAX) return fail(CG_EINVAL, "step index overflow");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (nsteps == 0) return CG_OK;
+  if (int rc = ensure_workspace(p)) return rc;
   if (!p->padded) return run_steps(p, state, step0, nsteps, first_bad, s);
   int rc;
   if ((rc = repack(p, state, p->nl, p->S0, p->ld, s))) return rc;

@@ -82,7 +82,7 @@ __device__ __forceinline__ void reaction(const double* k, double u, double v, do
     const double e4 = __ddiv_rn(MUL(MUL(e1, SUB(1.0, z5)), ADD(SUB(1.0, e3), MUL(e3, z5))),
                                 MUL(z5, ADD(1.0, MUL(e3, z5))));
     const double r = u, s = v;
-    const double pr = SUB(SUB(MUL(MUL(z2, SUB(1.0, s)), r), MUL(z3, MUL(MUL(r, r), r))), MUL(z4, SUB(s, z5)));
+    const double pr = SUB(SUB(MUL(MUL(z2, SUB(1.0, s)), r), MUL(z3, cube_rn(r))), MUL(z4, SUB(s, z5)));
     const double one_s = SUB(1.0, s);
     const double q1 = MUL(MUL(MUL(e1, ADD(1.0, MUL(e2, r))), one_s), SUB(1.0, MUL(e3, one_s)));
     const double q2 = MUL(MUL(MUL(e4, s), ADD(1.0, MUL(e3, s))), ADD(1.0, MUL(e5, r)));

@@ -36,7 +36,9 @@ def gather_fields(local, total: int, group=None, dst: int = 0):
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     biggest = max(shard_range(total, r, world)[1] - shard_range(total, r, world)[0] for r in range(world))
-    pad = torch.zeros((biggest,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    # gloo moves host tensors only: stage device blocks through host memory
+    dev = _comm_device(local.device, group)
+    pad = torch.zeros((biggest,) + tuple(local.shape[1:]), dtype=local.dtype, device=dev)
     pad[: local.shape[0]] = local
     bufs = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
     dist.gather(pad, bufs, dst=dst, group=group)
@@ -46,7 +48,33 @@ def gather_fields(local, total: int, group=None, dst: int = 0):
     for r in range(world):
         lo, hi = shard_range(total, r, world)
         parts.append(bufs[r][: hi - lo])
-    return torch.cat(parts, dim=0)
+    return torch.cat(parts, dim=0).to(local.device)
+
+
+def _comm_device(want, group=None):
+    """Device a collective's tensors must live on: the tensor's own for NCCL,
+    the host for gloo."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        return want if want.type == "cuda" else torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def agree(value: int, op: str, group=None) -> int:
+    """All-reduce one integer over the group (``op`` "min" or "max"); the
+    value itself when no process group is initialised.  Ranks use it to reach
+    the same decision (raise / continue) before any later collective, so a
+    rank-local error can never leave the others blocked in a gather."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return int(value)
+    t = torch.tensor([int(value)], dtype=torch.int64, device=_comm_device(torch.device("cpu"), group))
+    dist.all_reduce(t, op=dist.ReduceOp.MIN if op == "min" else dist.ReduceOp.MAX, group=group)
+    return int(t.item())
 
 
 def ensemble_plan(template, kin_kind: str, params: np.ndarray, tau: float, theta: str | None = None) -> SplitPlan:
@@ -121,23 +149,35 @@ class Ensemble:
         self.host_in = torch.empty(shape, dtype=torch.float64, pin_memory=True)
         self.host_out = torch.empty(shape, dtype=torch.float64, pin_memory=True)
         self.step = 0
+        # host_in may be rewritten only after the last upload has read it;
+        # host_out is valid once `downloaded` has completed
+        self.uploaded = torch.cuda.Event()
+        self.downloaded = torch.cuda.Event()
 
     @property
     def nbytes(self) -> int:
         return self.state.numel() * 8
 
     def load(self, host_states) -> None:
-        """Copy numpy/torch host states into the pinned buffer (outside any timing)."""
+        """Copy numpy/torch host states into the pinned buffer (outside any
+        timing).  Waits for the previous :meth:`advance`'s upload to have read
+        the buffer first, so a pending asynchronous copy never sees new data."""
         import torch
 
+        self.uploaded.synchronize()
         self.host_in.copy_(torch.as_tensor(np.ascontiguousarray(host_states)))
 
-    def advance(self, nsteps: int, *, from_host: bool = True, to_host: bool = True):
+    def advance(self, nsteps: int, *, from_host: bool = True, to_host: bool = True, blocking: bool = True):
         """Optionally upload host_in, step nsteps, optionally download to host_out.
 
         With a laned plan every lane uploads, steps and downloads its own run
         block on its own stream, so lane 1's upload runs under lane 0's
-        stepping and lane 0's download under lane 1's tail."""
+        stepping and lane 0's download under lane 1's tail.
+
+        Returns ``host_out``.  With ``blocking`` (default) the call returns
+        once the download has landed, so the buffer can be read at once; with
+        ``blocking=False`` it returns immediately and ``self.downloaded`` (a
+        CUDA event on the caller's stream) marks when host_out is valid."""
         import torch
 
         if from_host:
@@ -162,10 +202,14 @@ class Ensemble:
             for _, _, _, stream in lanes:
                 cur.wait_stream(stream)
         if from_host:
+            self.uploaded.record()
             self.step = 0
         self.step += nsteps
         if to_host and not lanes:
             self.host_out.copy_(self.state, non_blocking=True)
+        self.downloaded.record()
+        if to_host and blocking:
+            self.downloaded.synchronize()
         return self.host_out
 
 
@@ -223,18 +267,32 @@ def run_ensemble(systems, m: int, t_star: float, *, group=None, gather: bool = T
             sample_steps.append(min(m, (sample_steps[-1] // every + 1) * every))
     names = [c.name for c in systems[0].components]
     ncomp = len(names)
+    # Setup can fail on one shard only (a member with other components, an
+    # unsupported kinetics, a bad operator): every rank learns whether any
+    # failed before it steps, so none is left waiting in the final gather.
+    plan = None
+    setup_error = None
     if mine:
-        shared = _check_shared(mine)
-        kin = engine_kinetics(mine[0])
-        params = np.stack([engine_kinetics(s).param_vector() for s in mine])
-        if shared:
-            plan = ensemble_plan(mine[0], kin.kind, params, tau)
-        else:
-            # heterogeneous ensemble: one prepared operator set per (run, component)
-            geos = [prepare(c.ops, tau) for s in mine for c in s.components]
-            lifts = [float(getattr(c, "lift", 0.0)) for c in mine[0].components]
-            plan = SplitPlan(geos, batch=len(mine), kinetics=kin.kind, kin_params=params, lifts=lifts,
-                             ops_per_run=True)
+        try:
+            shared = _check_shared(mine)
+            kin = engine_kinetics(mine[0])
+            params = np.stack([engine_kinetics(s).param_vector() for s in mine])
+            if shared:
+                plan = ensemble_plan(mine[0], kin.kind, params, tau)
+            else:
+                # heterogeneous ensemble: one prepared operator set per (run, component)
+                geos = [prepare(c.ops, tau) for s in mine for c in s.components]
+                lifts = [float(getattr(c, "lift", 0.0)) for c in mine[0].components]
+                plan = SplitPlan(geos, batch=len(mine), kinetics=kin.kind, kin_params=params, lifts=lifts,
+                                 ops_per_run=True)
+        except Exception as exc:  # re-raised below, after the ranks agree
+            setup_error = exc
+    failed_rank = agree(rank if setup_error is not None else world, "min", group)
+    if failed_rank < world:
+        if setup_error is not None:
+            raise setup_error
+        raise RuntimeError(f"run_ensemble: setup failed on rank {failed_rank}; see that rank's error")
+    if mine:
         host = np.stack([np.stack([np.asarray(c.initial, dtype=np.float64) for c in s.components]) for s in mine])
         state = torch.from_numpy(np.ascontiguousarray(host)).to("cuda")
         first_bad = torch.full((hi - lo, plan.ncomp), INT32_MAX, dtype=torch.int32, device="cuda")
@@ -258,9 +316,11 @@ def run_ensemble(systems, m: int, t_star: float, *, group=None, gather: bool = T
         bad = np.zeros((0, len(systems[0].components)), dtype=np.int32)
         if sample_steps is not None:
             series = torch.zeros((0, ncomp, len(sample_steps)), dtype=torch.float64, device="cuda")
-    if raise_on_divergence and bad.size and bad.min() < INT32_MAX:
-        s = int(bad.min())
-        raise DivergenceError(f"ensemble run diverged at step {s}", step=s)
+    if raise_on_divergence:
+        # the first bad step over ALL ranks' runs, raised by every rank together
+        s = agree(int(bad.min()) if bad.size else INT32_MAX, "min", group)
+        if s < INT32_MAX:
+            raise DivergenceError(f"ensemble run diverged at step {s}", step=s)
     if dist_on and gather and world > 1:
         full = gather_fields(phys, R, group=group)
     else:

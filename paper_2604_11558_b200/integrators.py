@@ -229,7 +229,7 @@ import os as _os
 # How the periodic-theta factor Q diag(Phi) Q^T is applied: "gemm" = two dense
 # DMMA mu-mode products (the reference's formulation), "fft" = the exact
 # real-FFT propagator (csrc/thetafft.cuh).  Overridable per plan.
-THETA_MODE = _os.environ.get("CURVIGPU_THETA", "gemm")
+THETA_MODE = _os.environ.get("CURVIGPU_THETA", "fft")
 
 KINETICS_CODES = {
     "external": 0,
@@ -613,19 +613,26 @@ class RunResult:
 
 
 def engine_kinetics(system):
-    """The GPU kinetics descriptor of a system, or NotImplementedError for an
-    arbitrary Python closure (it cannot run on the device)."""
-    from .models import Kinetics
+    """The GPU descriptor of a system's reaction terms: a ``models.Kinetics``
+    (two-species systems) or ``models.BulkSurfaceCoupling`` (the
+    bulk-surface models).  Accepted forms, in order: the descriptor itself as
+    ``system.kinetics``; an ``engine_kinetics`` attribute; one of the
+    reference's own builder closures (``curvipat.models.build_system``
+    output: the descriptor is read from the closure, models.reference_kinetics).
+    Any other Python callable raises NotImplementedError (it cannot run on the
+    device, and there is no CPU fallback)."""
+    from .models import BulkSurfaceCoupling, Kinetics, reference_kinetics
 
-    kin = getattr(system, "kinetics", None)
-    if isinstance(kin, Kinetics):
-        return kin
-    kin = getattr(system, "engine_kinetics", None)
-    if isinstance(kin, Kinetics):
+    for kin in (getattr(system, "kinetics", None), getattr(system, "engine_kinetics", None)):
+        if isinstance(kin, (Kinetics, BulkSurfaceCoupling)):
+            return kin
+    kin = reference_kinetics(system)
+    if kin is not None:
         return kin
     raise NotImplementedError(
-        "system.kinetics is an arbitrary Python callable; the B200 engine needs a "
-        "paper_2604_11558_b200.models.Kinetics descriptor (no CPU fallback)")
+        "system.kinetics is a Python callable the engine cannot run on the GPU: pass a "
+        "paper_2604_11558_b200.models.Kinetics / BulkSurfaceCoupling descriptor (as system.kinetics or "
+        "system.engine_kinetics), or a system built by curvipat.models.build_system (no CPU fallback)")
 
 
 def _raise_if_diverged(bad, names):
@@ -701,14 +708,16 @@ def run_simulation(system, m: int, t_star: float, *, record_every: int | None = 
         raise ValueError(f"unknown method {method!r}")
     if method != "split":
         raise NotImplementedError("forward Euler is a reference comparison path, not part of the engine")
-    from .models import BulkSurfaceCoupling
+    from .models import BulkSurfaceCoupling, Kinetics
 
-    if isinstance(getattr(system, "kinetics", None), BulkSurfaceCoupling):
+    kin = engine_kinetics(system)
+    if isinstance(kin, BulkSurfaceCoupling):
         from .coupled import run_coupled
 
         return run_coupled(system, m, t_star, record_every=record_every, diagnostics=diagnostics,
-                           sample_hook=sample_hook, as_torch=as_torch)
-    kin = engine_kinetics(system)
+                           sample_hook=sample_hook, as_torch=as_torch, coupling=kin)
+    if not isinstance(kin, Kinetics):
+        raise NotImplementedError("two-species systems need a models.Kinetics descriptor")
     tau = t_star / m
     comps = list(system.components)
     names = [c.name for c in comps]

@@ -168,6 +168,81 @@ class BulkSurfaceCoupling:
 
 
 # ---------------------------------------------------------------------------
+# the reference's own built-in kinetics closures -> descriptors
+# ---------------------------------------------------------------------------
+
+# qualname of the closure each reference builder returns (models.py:491-661)
+_REFERENCE_CLOSURES = {
+    "_build_bvam.<locals>.kinetics": "bvam_disk",
+    "_build_anomalous.<locals>.kinetics": "schnakenberg_anomalous_disk",
+    "_build_dib_sphere.<locals>.kinetics": "dib_sphere",
+    "_build_ball.<locals>.kinetics": "bulk_surface_schnakenberg_ball",
+    "_build_cylinder.<locals>.kinetics": "bsdib_cylinder",
+}
+
+
+def _closure_cells(fn) -> dict:
+    names = getattr(getattr(fn, "__code__", None), "co_freevars", ())
+    cells = getattr(fn, "__closure__", None) or ()
+    out = {}
+    for n, c in zip(names, cells):
+        try:
+            out[n] = c.cell_contents
+        except ValueError:  # empty cell
+            pass
+    return out
+
+
+def descriptor_for_model(name, params: dict, h: float | None = None, rho_edge: float | None = None):
+    """The GPU descriptor of one of the reference's five built-in models
+    (what each builder's closure computes, models.py:491-661): a
+    :class:`Kinetics` for the two-species models, a
+    :class:`BulkSurfaceCoupling` for the bulk-surface ones (``h`` = h_rho or
+    h_z, ``rho_edge`` = last rho node of the ball)."""
+    name = ModelName(name) if isinstance(name, str) else ModelName(getattr(name, "value", name))
+    p = params
+    if name is ModelName.BVAM_DISK:
+        return Kinetics("bvam", {k: p[k] for k in KINETICS_PARAMS["bvam"]})
+    if name is ModelName.SCHNAKENBERG_ANOMALOUS_DISK:
+        return Kinetics("schnakenberg", {"gamma": p["alpha1"], "a": p["alpha2"], "b": p["beta1"]})
+    if name is ModelName.DIB_SPHERE:
+        return Kinetics("dib", {k: p[k] for k in KINETICS_PARAMS["dib"]})
+    if name is ModelName.BULK_SURFACE_SCHNAKENBERG_BALL:
+        return BulkSurfaceCoupling("ball", {k: p[k] for k in BULK_SURFACE_PARAMS["ball"]}, h=float(h),
+                                   rho_edge=float(rho_edge))
+    return BulkSurfaceCoupling("cylinder", {k: p[k] for k in BULK_SURFACE_PARAMS["cylinder"]}, h=float(h))
+
+
+def reference_kinetics(system):
+    """Descriptor for a system whose ``kinetics`` is one of the reference's
+    own builder closures (``curvipat.models.build_system`` output), read
+    from the closure itself -- its captured parameter map ``p`` and grid
+    constants (h_rho, rho_edge, h_z) -- and cross-checked against
+    ``system.spec``.  None for any other callable: an arbitrary Python
+    closure has no GPU kernel."""
+    fn = getattr(system, "kinetics", None)
+    model = _REFERENCE_CLOSURES.get(getattr(fn, "__qualname__", ""))
+    if model is None or not str(getattr(fn, "__module__", "")).endswith("models"):
+        return None
+    cells = _closure_cells(fn)
+    p = cells.get("p")
+    if not isinstance(p, dict):
+        return None
+    spec = getattr(system, "spec", None)
+    spec_name = getattr(getattr(spec, "name", None), "value", None)
+    if spec_name is not None and spec_name != model:
+        return None
+    try:
+        if model == "bulk_surface_schnakenberg_ball":
+            return descriptor_for_model(model, p, h=cells["h_rho"], rho_edge=cells["rho_edge"])
+        if model == "bsdib_cylinder":
+            return descriptor_for_model(model, p, h=cells["h_z"])
+        return descriptor_for_model(model, p)
+    except KeyError:
+        return None
+
+
+# ---------------------------------------------------------------------------
 # systems
 # ---------------------------------------------------------------------------
 
@@ -326,7 +401,7 @@ def build_system(spec, dims: dict, seed: int, overrides=None) -> CoupledSystem:
         theta = build_theta(dims["n_theta"])
         make = lambda k: ComponentOps(Geometry.DISK, k, rho=rho, theta=theta)  # noqa: E731
         comps = [_component(spec, "u", make(p["gamma"]), init), _component(spec, "v", make(p["delta"]), init)]
-        kin = Kinetics("bvam", {k: p[k] for k in KINETICS_PARAMS["bvam"]})
+        kin = descriptor_for_model(spec.name, p)
     elif spec.name is ModelName.SCHNAKENBERG_ANOMALOUS_DISK:
         lam = p["lambda"]
         rho = build_lambda(dims["n_rho"], spec.sizes["rho_star"], lam)
@@ -335,7 +410,7 @@ def build_system(spec, dims: dict, seed: int, overrides=None) -> CoupledSystem:
         make = lambda k: ComponentOps(Geometry.DISK, k, rho=rho, theta=theta, rho_weights=weights)  # noqa: E731
         comps = [_component(spec, "u", make(1.0), init, eq["u"]),
                  _component(spec, "v", make(p["delta"]), init, eq["v"])]
-        kin = Kinetics("schnakenberg", {"gamma": p["alpha1"], "a": p["alpha2"], "b": p["beta1"]})
+        kin = descriptor_for_model(spec.name, p)
     elif spec.name is ModelName.DIB_SPHERE:
         rs = spec.sizes["rho_star"]
         theta = build_theta(dims["n_theta"])
@@ -343,7 +418,7 @@ def build_system(spec, dims: dict, seed: int, overrides=None) -> CoupledSystem:
         make = lambda k: ComponentOps(Geometry.SPHERE, k, theta=theta, phi=phi)  # noqa: E731
         comps = [_component(spec, "r", make(1.0 / rs**2), init),
                  _component(spec, "s", make(p["epsilon"] / rs**2), init)]
-        kin = Kinetics("dib", {k: p[k] for k in KINETICS_PARAMS["dib"]})
+        kin = descriptor_for_model(spec.name, p)
     elif spec.name is ModelName.BULK_SURFACE_SCHNAKENBERG_BALL:
         # models.py:570-611
         rs = spec.sizes["rho_star"]
@@ -355,8 +430,7 @@ def build_system(spec, dims: dict, seed: int, overrides=None) -> CoupledSystem:
         comps = [_component(spec, "u", bulk(1.0), init), _component(spec, "v", bulk(p["delta"]), init),
                  _component(spec, "r", surf(1.0 / rs**2), init),
                  _component(spec, "s", surf(p["epsilon"] / rs**2), init)]
-        kin = BulkSurfaceCoupling("ball", {k: p[k] for k in BULK_SURFACE_PARAMS["ball"]},
-                                  h=float(rho.h), rho_edge=float(rho.grid[-1]))
+        kin = descriptor_for_model(spec.name, p, h=rho.h, rho_edge=rho.grid[-1])
     else:
         # models.py:614-661
         rho = build_rho(2, dims["n_rho"], spec.sizes["rho_star"])
@@ -367,7 +441,7 @@ def build_system(spec, dims: dict, seed: int, overrides=None) -> CoupledSystem:
         comps = [_component(spec, "u", bulk(1.0), init, eq["u"]),
                  _component(spec, "v", bulk(p["delta"]), init, eq["v"]),
                  _component(spec, "r", surf(1.0), init), _component(spec, "s", surf(p["epsilon"]), init)]
-        kin = BulkSurfaceCoupling("cylinder", {k: p[k] for k in BULK_SURFACE_PARAMS["cylinder"]}, h=float(z.h))
+        kin = descriptor_for_model(spec.name, p, h=z.h)
     return CoupledSystem(spec=spec, components=comps, kinetics=kin, equilibrium=eq)
 
 

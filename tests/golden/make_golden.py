@@ -43,6 +43,7 @@ import numpy as np  # noqa: E402
 
 HERE = Path(__file__).resolve().parent
 sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, str(HERE.parents[1]))
 
 from curvipat import models, tensor  # noqa: E402
 from curvipat import operators as op  # noqa: E402
@@ -65,104 +66,7 @@ SAMPLES = 4096
 # ---------------------------------------------------------------------------
 
 
-def _noise(seed, shape, bases, law):
-    rng = Xoshiro256pp(seed)
-    n = int(np.prod(shape))
-    out = []
-    for b in bases:
-        f = np.full(shape, b)
-        f += tensor.unvec(law.draw(rng, n), shape)
-        out.append(f)
-    return out
-
-
-def z_neumann(n, height):
-    h = height / (n - 1)
-    b = np.full(n - 1, 1.0 / h**2)
-    c = np.full(n - 1, 1.0 / h**2)
-    b[0] = c[-1] = 2.0 / h**2
-    return op.TridiagonalOperator(n=n, a=np.full(n, -2.0 / h**2), b=b, c=c, grid=h * np.arange(n), h=h,
-                                  kind=op.OperatorKind.Z)
-
-
-def ref_config(k, dims, seed=1):
-    spec = models.model_spec("bvam_disk")  # only read by diagnostics
-    if k == 1:
-        n1, n2 = dims
-        rho, th = op.build_rho(2, n1, 1.0), op.build_theta(n2)
-        u0, v0 = _noise(seed, (n1, n2), [1.0, 0.9], Uniform(-1e-3, 1e-3))
-        g, a, b = 100.0, 0.1, 0.9
-
-        def kin(s):
-            u, v = s["u"], s["v"]
-            uuv = u * u * v
-            return {"u": g * (a - u + uuv), "v": g * (b - uuv)}
-
-        comps = [SystemComponent("u", ComponentOps(Geometry.DISK, 1.0, rho=rho, theta=th), u0),
-                 SystemComponent("v", ComponentOps(Geometry.DISK, 10.0, rho=rho, theta=th), v0)]
-    elif k == 2:
-        n1, n2 = dims
-        th = op.build_theta(n1)
-        ph, _ = op.build_phi_op(n2)
-        A, B = 4.5, 6.96
-        u0, v0 = _noise(seed, (n1, n2), [A, B / A], Uniform(-1e-2, 1e-2))
-
-        def kin(s):
-            u, v = s["u"], s["v"]
-            uuv = u * u * v
-            return {"u": A - (B + 1.0) * u + uuv, "v": B * u - uuv}
-
-        comps = [SystemComponent("u", ComponentOps(Geometry.SPHERE, 0.01, theta=th, phi=ph), u0),
-                 SystemComponent("v", ComponentOps(Geometry.SPHERE, 0.08, theta=th, phi=ph), v0)]
-    elif k == 3:
-        n1, n2, n3 = dims
-        rho, th, z = op.build_rho(2, n1, 1.0), op.build_theta(n2), z_neumann(n3, 2.0)
-        rng = Xoshiro256pp(seed)
-        xi = rng.uniform(3)
-        rc, tc, zc = 0.5 * xi[0], 2.0 * np.pi * xi[1], 0.3 + 1.4 * xi[2]
-        n = n1 * n2 * n3
-        eu = tensor.unvec(Uniform(-1.0, 1.0).draw(rng, n), dims)
-        ev = tensor.unvec(Uniform(-1.0, 1.0).draw(rng, n), dims)
-        R, T, Z = np.meshgrid(rho.grid, th.grid, z.grid, indexing="ij")
-        inside = ((np.abs(R * np.cos(T) - rc * np.cos(tc)) <= 0.2)
-                  & (np.abs(R * np.sin(T) - rc * np.sin(tc)) <= 0.2) & (np.abs(Z - zc) <= 0.2))
-        u0 = np.where(inside, 0.5 * (1.0 + 0.01 * eu), 1.0)
-        v0 = np.where(inside, 0.25 * (1.0 + 0.01 * ev), 0.0)
-        F, kk = 0.04, 0.06
-
-        def kin(s):
-            u, v = s["u"], s["v"]
-            uvv = u * v * v
-            return {"u": -uvv + F * (1.0 - u), "v": uvv - (F + kk) * v}
-
-        comps = [SystemComponent("u", ComponentOps(Geometry.CYLINDER, 2e-5, rho=rho, theta=th, z=z), u0),
-                 SystemComponent("v", ComponentOps(Geometry.CYLINDER, 1e-5, rho=rho, theta=th, z=z), v0)]
-    elif k == 4:
-        n1, n2, n3 = dims
-        rho, th = op.build_rho(3, n1, 1.0), op.build_theta(n2)
-        ph, _ = op.build_phi_op(n3)
-        u0, v0 = _noise(seed, dims, [0.0, 0.0], Uniform(-1e-2, 1e-2))
-        eta, a, b, h, C = 0.45, 1.112, -1.01, -1.0, 0.02
-
-        def kin(s):
-            u, v = s["u"], s["v"]
-            uv = u * v
-            uvv = uv * v
-            return {"u": eta * (u + a * v - C * uv - uvv), "v": eta * (b * v + h * u + C * uv + uvv)}
-
-        comps = [SystemComponent("u", ComponentOps(Geometry.BALL, 0.516, rho=rho, theta=th, phi=ph), u0),
-                 SystemComponent("v", ComponentOps(Geometry.BALL, 1.0, rho=rho, theta=th, phi=ph), v0)]
-    else:
-        raise ValueError(k)
-    return CoupledSystem(spec=spec, components=comps, kinetics=kin, equilibrium={})
-
-
-def ref_member(i, dims, runs=512):
-    g = 50.0 + 150.0 * i / (runs - 1)
-    spec = models.model_spec("schnakenberg_anomalous_disk",
-                             {"alpha1": g, "alpha2": 0.1, "beta1": 0.9, "delta": 10.0})
-    return models.build_system(spec, {"n_rho": dims[0], "n_theta": dims[1]}, 1 + i)
-
+from oracle.ref_configs import _noise, ref_config, ref_member, z_neumann  # noqa: E402,F401
 
 STEPS = {1: (1000, 1.0), 2: (2000, 2.0), 3: (500, 250.0), 4: (1000, 10.0), 5: (1000, 1.0)}
 FULL = {1: (64, 128), 2: (512, 256), 3: (64, 128, 128), 4: (100, 100, 100), 5: (128, 256)}
@@ -414,6 +318,9 @@ CONVERGE_CASES = [
     {"model": "schnakenberg_anomalous_disk", "n_rho": 12, "n_theta": 16, "tstar": 0.002, "m_list": [5, 10, 20], "seed": 3},
     {"model": "bvam_disk", "n_rho": 10, "n_theta": 12, "tstar": 0.5, "m_list": [4, 8, 16], "m_ref": 96, "seed": 2},
     {"model": "dib_sphere", "n_theta": 12, "n_phi": 9, "tstar": 0.01, "m_list": [3, 6, 12], "seed": 5},
+    {"model": "bulk_surface_schnakenberg_ball", "n_rho": 6, "n_theta": 8, "n_phi": 6, "tstar": 0.002,
+     "m_list": [5, 10, 20], "seed": 4},
+    {"model": "bsdib_cylinder", "n_rho": 6, "n_theta": 8, "n_z": 5, "tstar": 0.05, "m_list": [4, 8, 16], "seed": 6},
 ]
 
 
