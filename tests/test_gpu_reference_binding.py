@@ -69,8 +69,10 @@ def test_cmd_run_outputs_match_reference(cli, monkeypatch, tmp_path, model, dims
         assert a.shape == b.shape, name
         assert np.array_equal(a[:, :-1 if name != "timeseries.csv" else 1], b[:, :-1 if name != "timeseries.csv"
                                                                               else 1]), name  # indices, grid, t
+        # north_star's tolerances: the step-0 snapshot is the initial state
+        # itself, later snapshots (steps 10..40) get the <= 1e-8 bound of 100 steps
+        tol = 0.0 if name.endswith("_0000000.csv") else 1e-8
         for col in range(a.shape[1] - 1 if name != "timeseries.csv" else 1, a.shape[1]):
-            tol = 1e-10 if name != "timeseries.csv" else 1e-9
             assert np.max(np.abs(a[:, col] - b[:, col])) <= tol * max(np.max(np.abs(a[:, col])), 1e-300), name
 
 
