@@ -176,6 +176,11 @@ int cg_plan_stage_info(const cg_plan* plan, int stage, long long* flops, long lo
 int cg_run_stage(cg_plan* plan, int stage, const double* W, double* W_out, int* first_bad, void* stream);
 /* Copy a plan workspace (0 = X, 1 = Y, 2 = second state) to dst (debugging / tests). */
 int cg_plan_copy_workspace(cg_plan* plan, int which, double* dst, void* stream);
+/* Bounds check (testing): a plan created with CURVIGPU_REDZONE=1 in the
+ * environment surrounds each workspace with a 1 MiB guard band of a fixed
+ * byte pattern; returns the number of guard bytes that were overwritten so
+ * far (0 = no out-of-bounds write), or < 0 on error.  Synchronises the device. */
+long long cg_plan_check_redzones(cg_plan* plan);
 
 /* step_split with external G plus the divergence guard: like cg_step, but the
  * guard records into first_bad with the plan's step counter, which this call

@@ -80,6 +80,7 @@ EXPORTS = (
     "cg_run_stage",
     "cg_plan_step_kernels",
     "cg_plan_copy_workspace",
+    "cg_plan_check_redzones",
     "cg_step_guarded",
     "cg_plan_set_step",
     "cg_coupling_create",
@@ -158,6 +159,8 @@ def lib():
     L.cg_plan_step_kernels.restype = ctypes.c_int
     L.cg_plan_copy_workspace.argtypes = [vp, ctypes.c_int, vp, vp]
     L.cg_plan_copy_workspace.restype = ctypes.c_int
+    L.cg_plan_check_redzones.argtypes = [vp]
+    L.cg_plan_check_redzones.restype = ctypes.c_longlong
     L.cg_step_guarded.argtypes = [vp, vp, vp, vp, vp, vp]
     L.cg_step_guarded.restype = ctypes.c_int
     L.cg_plan_set_step.argtypes = [vp, ctypes.c_longlong, vp]

@@ -377,6 +377,12 @@ struct cg_plan {
   double *coeff = nullptr, *lift = nullptr, *kin_params = nullptr;
   double *rho_b = nullptr, *phi_b = nullptr, *z_b = nullptr, *th = nullptr, *d_rho = nullptr, *d_phi = nullptr;
   double *X = nullptr, *Y = nullptr, *S2 = nullptr;
+  bool redzone = false;  // CURVIGPU_REDZONE: guard bands around the workspaces
+  struct Guarded {
+    uint8_t* raw;
+    size_t bytes;  // payload; kRedzone bytes of guard band on each side
+  };
+  std::vector<Guarded> guarded;
   int* step_dev = nullptr;
   int* scratch_bad = nullptr;
   std::vector<Stage> stages;
@@ -399,19 +405,38 @@ int dev_alloc(cg_plan* p, size_t bytes, void** out) {
 // X, Y, S2 (and S0 for padded storage), each the state's size: allocated by
 // the first entry point that touches them.  Not capture-safe by design: the
 // first call on a plan must not be made inside a caller's stream capture.
+// With CURVIGPU_REDZONE=1 in the environment every workspace gets a
+// kRedzone-byte guard band on both sides, filled with kRedzoneByte; a kernel
+// writing past a buffer lands in a band and cg_plan_check_redzones reports it
+// (our own bounds check: compute-sanitizer is not available on the GPU pool).
+constexpr size_t kRedzone = 1 << 20;
+constexpr unsigned char kRedzoneByte = 0xA5;
+
+int ws_alloc(cg_plan* p, size_t bytes, double** out) {
+  if (!p->redzone) return dev_alloc(p, bytes, reinterpret_cast<void**>(out));
+  uint8_t* raw = nullptr;
+  int rc = dev_alloc(p, bytes + 2 * kRedzone, reinterpret_cast<void**>(&raw));
+  if (rc) return rc;
+  CUDA_TRY(cudaMemset(raw, kRedzoneByte, bytes + 2 * kRedzone));
+  CUDA_TRY(cudaMemset(raw + kRedzone, 0, bytes));
+  *out = reinterpret_cast<double*>(raw + kRedzone);
+  p->guarded.push_back({raw, bytes});
+  return CG_OK;
+}
+
 int ensure_workspace(cg_plan* p) {
   if (p->X) return CG_OK;
   const size_t bytes = (size_t)p->elems * sizeof(double);
   int rc;
   double *X = nullptr, *Y = nullptr, *S2 = nullptr, *S0 = nullptr;
-  if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&X)))) return rc;
-  if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&Y)))) return rc;
-  if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&S2)))) return rc;
+  if ((rc = ws_alloc(p, bytes, &X))) return rc;
+  if ((rc = ws_alloc(p, bytes, &Y))) return rc;
+  if ((rc = ws_alloc(p, bytes, &S2))) return rc;
   if (p->padded) {
-    if ((rc = dev_alloc(p, bytes, reinterpret_cast<void**>(&S0)))) return rc;
+    if ((rc = ws_alloc(p, bytes, &S0))) return rc;
     for (double* buf : {X, Y, S2, S0}) CUDA_TRY(cudaMemset(buf, 0, bytes));
-    CUDA_TRY(cudaDeviceSynchronize());
   }
+  if (p->padded || p->redzone) CUDA_TRY(cudaDeviceSynchronize());
   p->Y = Y;
   p->S2 = S2;
   p->S0 = S0;
@@ -1199,6 +1224,10 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
   p->elems_u = p->npts_u * p->B * p->C;
   if (d->ops_per_run != 0 && d->ops_per_run != 1) return fail(CG_EINVAL, "ops_per_run must be 0 or 1");
   p->NO = d->ops_per_run ? p->B * p->C : p->C;
+  {
+    const char* rz = getenv("CURVIGPU_REDZONE");
+    p->redzone = rz && rz[0] && rz[0] != '0';
+  }
 
   int rc = CG_OK;
   auto bail = [&](int code) {
@@ -1306,6 +1335,23 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
 }
 
 int cg_plan_stage_count(const cg_plan* p) { return p ? (int)p->stages.size() : 0; }
+
+long long cg_plan_check_redzones(cg_plan* p) {
+  if (!p) return fail(CG_EINVAL, "null plan");
+  if (!p->redzone) return fail(CG_EINVAL, "plan was created without CURVIGPU_REDZONE=1");
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return fail(CG_ECUDA, cudaGetErrorString(e));
+  std::vector<unsigned char> h(kRedzone);
+  long long bad = 0;
+  for (const auto& g : p->guarded) {
+    for (const uint8_t* band : {g.raw, g.raw + kRedzone + g.bytes}) {
+      e = cudaMemcpy(h.data(), band, kRedzone, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return fail(CG_ECUDA, cudaGetErrorString(e));
+      for (unsigned char c : h) bad += c != kRedzoneByte;
+    }
+  }
+  return bad;
+}
 
 int cg_plan_copy_workspace(cg_plan* p, int which, double* dst, void* stream) {
   if (!p || !dst || which < 0 || which > 2) return fail(CG_EINVAL, "bad workspace request");

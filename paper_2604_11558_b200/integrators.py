@@ -464,6 +464,17 @@ class SplitPlan:
             _native.check(n, "cg_plan_step_kernels")
         return [ids[i] for i in range(min(n, 32))]
 
+    def check_redzones(self) -> int:
+        """Overwritten guard-band bytes around this plan's (and its lanes')
+        workspaces; the plan must have been created with CURVIGPU_REDZONE=1."""
+        total = 0
+        for h in [self._h] + [sub._h for _, _, sub, _ in self._lanes]:
+            n = int(self._lib.cg_plan_check_redzones(h))
+            if n < 0:
+                _native.check(n, "cg_plan_check_redzones")
+            total += n
+        return total
+
     def workspace(self, which: int):
         """Copy of workspace X (0), Y (1) or the second state buffer (2)."""
         import torch
