@@ -399,6 +399,12 @@ __device__ __forceinline__ void dft_any(double2* a) {
   }
 }
 
+#ifdef CURVIGPU_TAIL_CTA_SYNC
+constexpr bool kTailCtaSync = true;   // A/B build: CTA barriers around the line transposes
+#else
+constexpr bool kTailCtaSync = false;
+#endif
+
 template <int M1, int M2, int NT = 256>
 struct FastTheta {
   static constexpr int M = M1 * M2;
@@ -496,7 +502,13 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
       wearly[k2] = make_double2(__ldg(p.Wprev + o0), __ldg(p.Wprev + o0 + es));
     }
   }
-  __syncthreads();
+  // RS lines live in one warp and S is private to a line, so the transposes
+  // only need warp-level ordering: the CTA's warps then drift apart and one
+  // warp's shared-memory phases run under another's FP64 phases
+  if constexpr (RS && !kTailCtaSync)
+    __syncwarp();
+  else
+    __syncthreads();
   if constexpr (RS) {
     static_assert(TPL == M1 && (TPL & (TPL - 1)) == 0 && TPL <= 32 && M2 % 2 == 0, "register split layout");
     constexpr int H = M2 / 2;
@@ -545,7 +557,11 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
       // slot M2 - 1 - h: from the partner, or (lt = 0) own pair h + 1 / the M/2 self pair
       keep[M2 - 1 - h] = z0 ? (h + 1 < H ? out_hi[h + 1] : selfm) : back;
     }
-    __syncthreads();  // every thread has read its S row (phase B) before phase A overwrites S
+    // every thread has read its S row (phase B) before phase A overwrites S
+    if constexpr (kTailCtaSync)
+      __syncthreads();
+    else
+      __syncwarp();
     // ---------------- inverse phase A from registers: column n2 = lt + q M1 holds k2 = q + (M2/M1) n1
 #pragma unroll
     for (int q = 0; q < M2 / TPL; ++q) {
@@ -623,7 +639,10 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
       phase_a<M1, M2, true>(keepa[q], S, lt + q * TPL, tw);
   }
   }  // RS
-  __syncthreads();
+  if constexpr (RS && !kTailCtaSync)
+    __syncwarp();
+  else
+    __syncthreads();
   // ---------------- inverse phase B + store (y_2k = Re z'_k / M, y_2k+1 = Im z'_k / M)
   // With a compile-time layout (BCM != 0) the axpy epilogue's W values are
   // loaded before the row's shared-memory loads and inverse DFT, so their L2
