@@ -240,6 +240,36 @@ int cg_coupled_kinetics(cg_coupling* c, const double* Wb, const double* Ws, doub
 int cg_coupled_run(cg_coupling* c, cg_plan* bulk, cg_plan* surf, double* Wb, double* Ws, long long step0,
                    long long nsteps, int* first_bad, void* stream);
 
+/* ---- on-device setup ----
+ * Batched device replacements for the per-operator host work of prepare()
+ * (integrators.py:130-173), for ensembles whose runs do not share operators.
+ * All pointers are DEVICE pointers; calls are stream-ordered and
+ * graph-capturable; nothing synchronises the host.
+ *
+ * cg_setup_eig_tridiag   replaces eig_tridiag()  operators.py:371-382 with the
+ *   symmetriser symmetrize() operators.py:357-368 (scipy/LAPACK there): nmat
+ *   operators with bands a [nmat][n], b, c [nmat][n-1] (b, c > 0) ->
+ *   lam [nmat][n] ascending, Qt [nmat][n][n] with Qt[k][r] = Q[r][k]
+ *   (eigenvector k contiguous, orthonormal), xi [nmat][n] the symmetriser
+ *   (V = diag(xi) Q, V^-1 = Q^T diag(1/xi)).  work: nmat*n*n doubles of
+ *   scratch (distinct from Qt).  status [nmat]: 0 ok, 1 the QL iteration did
+ *   not converge (NumericalFailure, operators.py:381), 2 a nonpositive
+ *   off-diagonal (ValueError, operators.py:362).
+ * cg_setup_phi1_matrix   replaces phi1_matrix()  phifun.py:68-71:
+ *   out[set] = V diag(phi1(s[set] * lam)) V^-1 for nset (operator, scale)
+ *   pairs; mat_of_set[set] picks the operator (NULL: set itself).
+ * cg_setup_phi1_outer    replaces phi1_outer()   phifun.py:52-65:
+ *   out[set][i][j][k] = phi1(s[set] * ((f1[set][i] * f2[set][j]) * f3[set][k])),
+ *   f3 NULL (n3 = 1) for two factors.
+ * cg_setup_phi1          replaces phi1()         phifun.py:23-37, elementwise. */
+int cg_setup_eig_tridiag(int nmat, int n, const double* a, const double* b, const double* c, double* lam, double* Qt,
+                         double* xi, double* work, int* status, void* stream);
+int cg_setup_phi1_matrix(int nset, int n, const double* lam, const double* Qt, const double* xi,
+                         const int* mat_of_set, const double* s, double* out, void* stream);
+int cg_setup_phi1_outer(int nset, int n1, int n2, int n3, const double* f1, const double* f2, const double* f3,
+                        const double* s, double* out, void* stream);
+int cg_setup_phi1(long long count, const double* x, double* out, void* stream);
+
 /* Last error message of the calling thread. */
 const char* cg_last_error(void);
 int cg_version(void);

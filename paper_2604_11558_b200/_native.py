@@ -89,6 +89,10 @@ EXPORTS = (
     "cg_coupled_run",
     "cg_weighted_sums_scratch",
     "cg_weighted_sums",
+    "cg_setup_eig_tridiag",
+    "cg_setup_phi1_matrix",
+    "cg_setup_phi1_outer",
+    "cg_setup_phi1",
 )
 
 CG_BS_BALL = 1
@@ -178,6 +182,15 @@ def lib():
     L.cg_weighted_sums.argtypes = [vp, ctypes.c_longlong, ctypes.c_longlong, vp, ctypes.c_int, vp, vp, vp,
                                    ctypes.c_longlong, vp]
     L.cg_weighted_sums.restype = ctypes.c_int
+    ci = ctypes.c_int
+    L.cg_setup_eig_tridiag.argtypes = [ci, ci, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.cg_setup_eig_tridiag.restype = ci
+    L.cg_setup_phi1_matrix.argtypes = [ci, ci, vp, vp, vp, vp, vp, vp, vp]
+    L.cg_setup_phi1_matrix.restype = ci
+    L.cg_setup_phi1_outer.argtypes = [ci, ci, ci, ci, vp, vp, vp, vp, vp, vp]
+    L.cg_setup_phi1_outer.restype = ci
+    L.cg_setup_phi1.argtypes = [ctypes.c_longlong, vp, vp, vp]
+    L.cg_setup_phi1.restype = ci
     _lib = L
     return L
 

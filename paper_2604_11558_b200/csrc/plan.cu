@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "curvigpu.h"
+#include "errors.h"
 #include "gemm.cuh"
 #include "stencil.cuh"
 #include "thetafft.cuh"
@@ -47,6 +48,13 @@ int fail(int code, const std::string& msg) {
       return fail(CG_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_) + " @" + \
                                 std::to_string(__LINE__));                                  \
   } while (0)
+
+}  // namespace
+
+// other translation units (setup.cu) report through the same thread-local message
+int cg_internal_fail(int code, const char* msg) { return fail(code, msg ? msg : ""); }
+
+namespace {
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,

@@ -227,7 +227,7 @@ class EnsembleResult:
 
 def run_ensemble(systems, m: int, t_star: float, *, group=None, gather: bool = True,
                  as_torch: bool = False, raise_on_divergence: bool = False,
-                 record_every: int | None = None, diagnostics=None) -> EnsembleResult:
+                 record_every: int | None = None, diagnostics=None, setup: str = "host") -> EnsembleResult:
     """Advance every member of ``systems`` (a list of CoupledSystem on one
     grid) by m steps of tau = t*/m; shard over the torch.distributed group
     when one is initialised.  Members sharing their operators run on one
@@ -238,7 +238,12 @@ def run_ensemble(systems, m: int, t_star: float, *, group=None, gather: bool = T
     ``mean_diagnostics(systems[0])``) samples every member's integral means on
     the device at step 0, every ``record_every`` steps and at m, as
     run_simulation does for one run; the [R, C, nsamples] series is gathered
-    with the fields."""
+    with the fields.
+
+    ``setup``: where a heterogeneous ensemble's per-run operator sets are
+    prepared -- ``"host"`` (``prepare`` per run and component, the reference's
+    path) or ``"device"`` (``device_setup.prepare_device``: every eigenproblem
+    and phi1 table of the shard in batched GPU launches)."""
     import torch
     import torch.distributed as dist
 
@@ -246,6 +251,8 @@ def run_ensemble(systems, m: int, t_star: float, *, group=None, gather: bool = T
         raise ValueError("need at least one time step")
     if t_star <= 0:
         raise ValueError("t_star must be positive")
+    if setup not in ("host", "device"):
+        raise ValueError(f"setup must be 'host' or 'device', got {setup!r}")
     R = len(systems)
     if R == 0:
         raise ValueError("empty ensemble")
@@ -281,7 +288,12 @@ def run_ensemble(systems, m: int, t_star: float, *, group=None, gather: bool = T
                 plan = ensemble_plan(mine[0], kin.kind, params, tau)
             else:
                 # heterogeneous ensemble: one prepared operator set per (run, component)
-                geos = [prepare(c.ops, tau) for s in mine for c in s.components]
+                if setup == "device":
+                    from .device_setup import prepare_device
+
+                    geos = prepare_device([c.ops for s in mine for c in s.components], tau)
+                else:
+                    geos = [prepare(c.ops, tau) for s in mine for c in s.components]
                 lifts = [float(getattr(c, "lift", 0.0)) for c in mine[0].components]
                 plan = SplitPlan(geos, batch=len(mine), kinetics=kin.kind, kin_params=params, lifts=lifts,
                                  ops_per_run=True)
