@@ -24,6 +24,7 @@
 #include "curvigpu.h"
 #include "errors.h"
 #include "gemm.cuh"
+#include "resident.cuh"
 #include "stencil.cuh"
 #include "thetafft.cuh"
 #include "fused_disk.cuh"
@@ -349,6 +350,11 @@ struct Stage {
   int phi_m, phi_n, phi_rdiv;
   CUtensorMap opmap;  // operator operand (B for TN, A for NN)
   CUtensorMap opmap2;  // EPI_CHAIN: the second operator (B2, TN layout)
+  // resident-operator kernel (resident.cuh): 8-row blocks of the operator
+  // extent (0 = the tiled kernel runs this stage), k steps, padded operator copies
+  int res_nb, res_ks;
+  const double* rop;
+  const double* rop2;
   // VAR_THETA: field = [A][N][Bc], W lines per CTA, Phi_j table, twiddles
   int tA, tBc, tW, tclass_mode, tnclass;
   const double* phif;
@@ -487,6 +493,93 @@ int upload_operator(cg_plan* p, int var, int n, Get get, double** out, CUtensorM
   return make_map(map, *out, 3, dims, strides, box);
 }
 
+// ---- resident-operator stages (resident.cuh) ----
+template <int VAR, int EPI, int NB, int KSTEPS>
+int launch_resident_t(const ResParams& rp, cudaStream_t s, bool conf) {
+  auto kern = resident_gemm_kernel<VAR, EPI, NB, KSTEPS>;
+  constexpr size_t smem = res_smem_bytes<EPI, NB, KSTEPS>();
+  if (conf) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    return CG_OK;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const long long units = (long long)rp.nitems * rp.upi;
+  const unsigned blocks = (unsigned)std::min<long long>(sms, (units + kResGroups - 1) / kResGroups);
+  return launch_pdl(kern, dim3(blocks), dim3(kResWarps * 32), smem, s, rp);
+}
+
+template <int VAR, int EPI>
+int launch_resident_s(int nb, const ResParams& rp, cudaStream_t s, bool conf) {
+  if (nb == 8) return launch_resident_t<VAR, EPI, 8, 16>(rp, s, conf);
+  if (nb == 13) return launch_resident_t<VAR, EPI, 13, 25>(rp, s, conf);
+  if constexpr (EPI != EPI_CHAIN) {
+    if (nb == 16) return launch_resident_t<VAR, EPI, 16, 32>(rp, s, conf);
+  }
+  return fail(CG_EUNSUPPORTED, "no resident-operator instantiation for this extent");
+}
+
+int launch_resident(int var, int epi, int nb, const ResParams& rp, cudaStream_t s, bool conf = false) {
+  if (var == VAR_TN) {
+    if (epi == EPI_STORE) return launch_resident_s<VAR_TN, EPI_STORE>(nb, rp, s, conf);
+    if (epi == EPI_PHI) return launch_resident_s<VAR_TN, EPI_PHI>(nb, rp, s, conf);
+    if (epi == EPI_CHAIN) return launch_resident_s<VAR_TN, EPI_CHAIN>(nb, rp, s, conf);
+  } else {
+    if (epi == EPI_STORE) return launch_resident_s<VAR_NN, EPI_STORE>(nb, rp, s, conf);
+    if (epi == EPI_PHI) return launch_resident_s<VAR_NN, EPI_PHI>(nb, rp, s, conf);
+    if (epi == EPI_AXPY) return launch_resident_s<VAR_NN, EPI_AXPY>(nb, rp, s, conf);
+  }
+  return fail(CG_EUNSUPPORTED, "no resident-operator kernel for this stage");
+}
+
+// 8-row blocks of the resident instantiation that fits an n x n operator (0: none)
+int resident_blocks(int epi, int n) {
+  if (n <= 64) return 8;
+  if (n <= 100) return 13;
+  if (n <= 128 && epi != EPI_CHAIN) return 16;
+  return 0;
+}
+int resident_ksteps(int nb) { return nb == 8 ? 16 : nb == 13 ? 25 : 32; }
+
+// Should a stage run the resident-operator kernel?  Measured on B200
+// (profiles/r02_resident_kernels.txt, tools/kernel_times.py): the ball's
+// chained polar pair gains (45.7 -> 35.4 us: its two operators stay resident,
+// the intermediate stays on chip and half-strip units balance n = 100), the
+// single products do not (ball rho 22.4 vs 21.5 us tiled, cylinder phi1_z 21.4
+// vs 21.0, cylinder rho 15.6 vs 13.0, config 5 rho 358 vs 277: one operator
+// fragment load per DMMA and X loads that all warps of a sub-partition wait
+// for at the same time hold the DMMA pipe at 66 %), so only chained stages take
+// it by default.  CURVIGPU_RESIDENT=0 disables it, =1 takes every eligible
+// stage (measurement; the parity suite runs in both modes).
+bool want_resident(int var, int epi, long long nitems, int M, int N, int K, int n_op) {
+  const char* env = getenv("CURVIGPU_RESIDENT");
+  if (env && env[0] == '0') return false;
+  if (K != n_op || (var == VAR_TN ? N != n_op : M != n_op)) return false;
+  if (!resident_blocks(epi, n_op)) return false;
+  // CURVIGPU_RESIDENT_CHAIN_ONLY=1 with =1: force the chained stages only (tests at small sizes)
+  if (env && env[0] == '1') return epi == EPI_CHAIN || !getenv("CURVIGPU_RESIDENT_CHAIN_ONLY");
+  const long long units = nitems * (((var == VAR_TN ? M : N) + 7) / 8);
+  return epi == EPI_CHAIN && units >= 2LL * 4 * 148;
+}
+
+// zero-padded row-major copy [NO][8 nb][LDS] of the n x n operators L_c[r][q] = get(c, r, q)
+template <typename Get>
+int upload_resident_operator(cg_plan* p, int n, int nb, Get get, const double** out) {
+  const int lds = res_lds(resident_ksteps(nb));
+  std::vector<double> h((size_t)p->NO * nb * 8 * lds, 0.0);
+  for (int c = 0; c < p->NO; ++c)
+    for (int r = 0; r < n; ++r)
+      for (int q = 0; q < n; ++q) h[((size_t)c * nb * 8 + r) * lds + q] = get(c, r, q);
+  double* d = nullptr;
+  int rc = upload(p, h.data(), h.size(), &d);
+  *out = d;
+  return rc;
+}
+
 int pick_cfg(int var, long long nbatch, int M, int N, int K, int stage_index) {
   // measurement override: CURVIGPU_TILE_CFG=<cfg> or "<s0>,<s1>,..." per stage
   if (const char* env = getenv("CURVIGPU_TILE_CFG")) {
@@ -566,6 +659,11 @@ int add_stage(cg_plan* p, int var, int epi, int M, int N, int K, int nslab, int 
   const int box_rows = (var == VAR_TN) ? kCfgs[st.cfg].BN : 16;
   int rc = upload_operator(p, var, n_op, get, &op, &st.opmap, box_rows);
   if (rc) return rc;
+  if (want_resident(var, epi, nbatch, st.M, st.N, st.K, n_op)) {
+    st.res_nb = resident_blocks(epi, n_op);
+    st.res_ks = resident_ksteps(st.res_nb);
+    if ((rc = upload_resident_operator(p, n_op, st.res_nb, get, &st.rop))) return rc;
+  }
   p->stages.push_back(st);
   return CG_OK;
 }
@@ -574,7 +672,9 @@ double* buf_ptr(cg_plan* p, int id, double* out) { return id == BUF_X ? p->X : i
 
 bool pow2(int n) { return n >= 4 && (n & (n - 1)) == 0; }
 // theta extents the FFT propagator handles: powers of two, and 100 (M = 5 x 10)
-bool fft_extent(int n) { return pow2(n) || n == 100; }
+// (the 100-point kernel takes 20 lines per CTA: `span`, the extent the lines are
+// spread over, must be a multiple of 20 -- other spans keep the GEMM pair)
+bool fft_extent(int n, int span) { return pow2(n) || (n == 100 && span % 20 == 0); }
 
 // row stride of the scaled Phi table: M + 1 rounded up to a multiple of 8
 // doubles that is an odd multiple of 8 (two lines 64 bytes apart per half-warp)
@@ -754,6 +854,35 @@ int launch_theta(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
 int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, int* first_bad, cudaStream_t s) {
   int rc;
   if (st.var == VAR_THETA) return launch_theta(p, st, Win, Wout, first_bad, s);
+  if (st.res_nb) {
+    ResParams rp{};
+    rp.M = st.M;
+    rp.N = st.N;
+    rp.K = st.K;
+    rp.nslab = st.nslab;
+    rp.ncomp = p->NO;
+    rp.nitems = p->B * p->C * st.nslab;
+    rp.upi = ((st.var == VAR_TN ? st.M : st.N) + 7) / 8;
+    rp.ldr = st.ldr;
+    rp.fstride = p->npts;
+    rp.sstride = st.var == VAR_NN ? (long long)st.K * st.ldr : 0;
+    rp.X = buf_ptr(p, st.src, Wout);
+    rp.out = buf_ptr(p, st.dst, Wout);
+    rp.w = Win;
+    rp.op = st.rop;
+    rp.op2 = st.rop2;
+    rp.phi = st.phi;
+    rp.phi_c = st.phi_c;
+    rp.phi_s = st.phi_s;
+    rp.phi_m = st.phi_m;
+    rp.phi_n = st.phi_n;
+    rp.phi_rdiv = st.phi_rdiv;
+    rp.tau = p->tau;
+    rp.limit = 1e12;  // DIVERGENCE_LIMIT, integrators.py:33
+    rp.first_bad = first_bad;
+    rp.step = p->step_dev;
+    return launch_resident(st.var, st.epi, st.res_nb, rp, s);
+  }
   {
     const double* src = buf_ptr(p, st.src, Wout);
     double* dst = buf_ptr(p, st.dst, Wout);
@@ -1046,13 +1175,17 @@ int build_stages(cg_plan* p, const cg_desc* d) {
     if (chain) {
       double* op2 = nullptr;
       *cur = BUF_Y;
+      if (s0.res_nb) {
+        int r3 = upload_resident_operator(p, n3, s0.res_nb, get_v, &s0.rop2);
+        if (r3) return r3;
+      }
       return upload_operator(p, VAR_TN, n3, get_v, &op2, &s0.opmap2, kCfgs[chain_cfg].BN);
     }
     *cur = BUF_X;
     return add_stage(p, VAR_TN, EPI_STORE, n1 * n2, n3, n3, 1, BUF_Y, BUF_X, n3, get_v);
   };
   auto other = [](int b) { return b == BUF_X ? BUF_Y : BUF_X; };
-  if (p->geom == CG_BALL && fft && fft_extent(n2)) {
+  if (p->geom == CG_BALL && fft && fft_extent(n2, n3)) {
     if ((rc = need(d->phi1_rho, "phi1_rho")) || (rc = need(d->Phi, "Phi")) ||
         (rc = need(d->Phi_outer, "Phi_outer")) || (rc = need(d->V_phi, "V_phi")) ||
         (rc = need(d->Vinv_phi, "Vinv_phi")))
@@ -1281,6 +1414,11 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
   if ((rc = setup_fused_front(p))) return bail(rc);
   for (const Stage& st : p->stages) {
     if (st.var == VAR_THETA) continue;
+    if (st.res_nb) {
+      ResParams rp{};
+      if ((rc = launch_resident(st.var, st.epi, st.res_nb, rp, nullptr, true))) return bail(rc);
+      continue;
+    }
     Maps dummy{};
     GemmParams gp{};
     if ((rc = launch_gemm(st.var, st.epi, st.cfg, dummy, gp, nullptr, true))) return bail(rc);

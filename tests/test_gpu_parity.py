@@ -508,3 +508,18 @@ def test_ball_chained_polar_products_match_two_stages_bitwise(monkeypatch, theta
         ref = orc.integrate(osys, 25, 25 * tau)
         for i, c in enumerate(sysm.components):
             assert rel_inf(outs[0][0, i], ref[c.name]) <= STEP1_TOL, c.name
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims", [(12, 100, 24), (6, 100, 20), (6, 100, 8)])
+def test_ball_with_100_theta_points_and_any_polar_extent_matches_the_oracle(dims):
+    """n_theta = 100 takes the 5 x 10 FFT only when the polar extent fills its
+    20-line CTAs; other extents must keep the GEMM pair (a 100-point line
+    once fell through to the power-of-two Stockham kernel)."""
+    from paper_2604_11558_b200.integrators import run_simulation
+
+    got = run_simulation(pcfg.BUILDERS[4](dims), 4, 0.04).fields
+    osys = ocfg.BUILDERS[4](dims)
+    ref = orc.physical(osys, orc.integrate(osys, 4, 0.04))
+    for name in ref:
+        assert rel_inf(got[name], ref[name]) <= 1e-12, (dims, name)

@@ -45,14 +45,16 @@ def stage_output(plan, st, W, out):
 
 def main():
     os.environ["CURVIGPU_LANES"] = "1"
-    for cfg in (None, "2", "7", "8", "9", "11", "12", "13", "15"):
-        if cfg:
+    for cfg in (None, "resident", "2", "7", "8", "9", "11", "12", "13", "15"):
+        os.environ.pop("CURVIGPU_TILE_CFG", None)
+        os.environ.pop("CURVIGPU_RESIDENT", None)
+        if cfg == "resident":  # every eligible stage through the resident-operator kernel
+            os.environ["CURVIGPU_RESIDENT"] = "1"
+        elif cfg:
             os.environ["CURVIGPU_TILE_CFG"] = cfg
-        else:
-            os.environ.pop("CURVIGPU_TILE_CFG", None)
         for k in (1, 2, 3, 4, 5):
             for theta in ("fft", "gemm"):
-                if cfg and k == 5:
+                if cfg and cfg != "resident" and k == 5:
                     continue
                 plan, W = plan_for(k, theta)
                 out = torch.empty_like(W)
