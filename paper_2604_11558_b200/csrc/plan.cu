@@ -28,6 +28,7 @@
 #include "stencil.cuh"
 #include "thetafft.cuh"
 #include "fused_disk.cuh"
+#include "cluster_disk.cuh"
 #include "coupling.cuh"
 #include "diagnostics.cuh"
 
@@ -406,6 +407,10 @@ struct cg_plan {
   // as one persistent fused kernel (fused_disk.cuh) inside cg_run
   bool fused_front = false;
   int fused_m1 = 0, fused_m2 = 0, fused_nt = 256;
+  // small disks (config 1): cg_run advances all its steps in one cluster
+  // kernel with the state in the cluster's shared memory (cluster_disk.cuh)
+  bool cluster_step = false;
+  const double* cluster_rop = nullptr;
 };
 
 namespace {
@@ -1002,9 +1007,9 @@ int launch_fused_k(int kin, const ThetaParams& tp, const StencilParams& sp, cuda
   }
 }
 
-int launch_fused_front(cg_plan* p, const double* Win, bool count_step, cudaStream_t s, bool conf = false) {
+void fill_front_params(cg_plan* p, const double* Win, bool count_step, ThetaParams& tp, StencilParams& sp) {
   const Stage& st = p->stages[0];
-  ThetaParams tp{};
+  tp = ThetaParams{};
   tp.N = st.N;
   tp.A = st.tA;
   tp.Bc = 1;
@@ -1018,7 +1023,7 @@ int launch_fused_front(cg_plan* p, const double* Win, bool count_step, cudaStrea
   tp.phis_ld = st.phis_ld;
   tp.tw = st.tw;
   tp.Y = buf_ptr(p, st.dst, nullptr);
-  StencilParams sp{};
+  sp = StencilParams{};
   sp.geometry = p->geom;
   sp.n1 = p->n1;
   sp.n2 = p->n2;
@@ -1036,6 +1041,12 @@ int launch_fused_front(cg_plan* p, const double* Win, bool count_step, cudaStrea
   sp.nparams = p->P;
   sp.W = Win;
   sp.step = count_step ? p->step_dev : nullptr;
+}
+
+int launch_fused_front(cg_plan* p, const double* Win, bool count_step, cudaStream_t s, bool conf = false) {
+  ThetaParams tp;
+  StencilParams sp;
+  fill_front_params(p, Win, count_step, tp, sp);
   if (p->fused_m1 == 8 && p->fused_m2 == 16) return launch_fused_k<8, 16>(p->kin, tp, sp, s, conf, p->fused_nt);
   if (p->fused_m1 == 8 && p->fused_m2 == 8) return launch_fused_k<8, 8>(p->kin, tp, sp, s, conf, p->fused_nt);
   return launch_fused_k<4, 8>(p->kin, tp, sp, s, conf, p->fused_nt);
@@ -1101,6 +1112,100 @@ int setup_fused_front(cg_plan* p) {
   int rc = launch_fused_front(p, nullptr, false, nullptr, true);
   if (rc) return rc;
   p->fused_front = true;
+  return CG_OK;
+}
+
+// ---- small disks: many steps in one cluster kernel (cluster_disk.cuh) ----
+void fill_front_params(cg_plan* p, const double* Win, bool count_step, ThetaParams& tp, StencilParams& sp);
+
+template <int M1, int M2, int KIN>
+int launch_cluster_t(const ClusterDiskParams& cp, int batch, cudaStream_t s, bool conf) {
+  using D = ClusterDisk<M1, M2>;
+  auto kern = disk_cluster_kernel<M1, M2, KIN>;
+  if (conf) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D::smem));
+    if (D::NC > 8) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(batch * D::NC));
+  cfg.blockDim = dim3(D::NT);
+  cfg.dynamicSmemBytes = D::smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = D::NC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (conf) {
+    // the cluster must be schedulable on this device (16 CTAs of ~115 KB on one GPC)
+    int nclusters = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg);
+    if (e != cudaSuccess || nclusters < 1) {
+      cudaGetLastError();
+      return fail(CG_EUNSUPPORTED, "cluster step kernel is not schedulable on this device");
+    }
+    return CG_OK;
+  }
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, cp));
+  return CG_OK;
+}
+
+template <int M1, int M2>
+int launch_cluster_k(int kin, const ClusterDiskParams& cp, int batch, cudaStream_t s, bool conf) {
+  switch (kin) {
+    case KIN_SCHNAKENBERG: return launch_cluster_t<M1, M2, KIN_SCHNAKENBERG>(cp, batch, s, conf);
+    case KIN_BRUSSELATOR: return launch_cluster_t<M1, M2, KIN_BRUSSELATOR>(cp, batch, s, conf);
+    case KIN_GRAY_SCOTT: return launch_cluster_t<M1, M2, KIN_GRAY_SCOTT>(cp, batch, s, conf);
+    case KIN_BVAM_ETA: return launch_cluster_t<M1, M2, KIN_BVAM_ETA>(cp, batch, s, conf);
+    case KIN_BVAM: return launch_cluster_t<M1, M2, KIN_BVAM>(cp, batch, s, conf);
+    default: return launch_cluster_t<M1, M2, KIN_DIB>(cp, batch, s, conf);
+  }
+}
+
+int launch_cluster_steps(cg_plan* p, double* state, long long step0, long long nsteps, int* first_bad,
+                         cudaStream_t s, bool conf = false) {
+  ClusterDiskParams cp{};
+  fill_front_params(p, state, false, cp.tp, cp.sp);
+  cp.rop = p->cluster_rop;
+  cp.state = state;
+  cp.step0 = (int)step0;
+  cp.nsteps = (int)nsteps;
+  cp.tau = p->tau;
+  cp.limit = 1e12;  // DIVERGENCE_LIMIT, integrators.py:33
+  cp.first_bad = first_bad;
+  if (p->n2 == 128) return launch_cluster_k<8, 8>(p->kin, cp, p->B, s, conf);
+  return launch_cluster_k<4, 8>(p->kin, cp, p->B, s, conf);
+}
+
+// Eligible: the fused front applies (disk, two species, built-in kinetics, FFT
+// theta), the grid is one of the cluster shapes (n_rho = 4 * n_theta / 8:
+// 64 x 128 -- config 1 -- or 32 x 64) and every run gets its own cluster at
+// once (B * NC <= SMs: a latency-bound plan; larger batches fill the chip
+// through the batched kernels).  CURVIGPU_NO_CLUSTER_STEP=1 keeps the
+// two-kernel step (measurement / A-B tests).
+int setup_cluster_step(cg_plan* p, const cg_desc* d) {
+  if (!p->fused_front || getenv("CURVIGPU_NO_CLUSTER_STEP") || !d->phi1_rho) return CG_OK;
+  if (!((p->n1 == 64 && p->n2 == 128) || (p->n1 == 32 && p->n2 == 64))) return CG_OK;
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int nc = p->n2 / 8;
+  if ((long long)p->B * nc > sms) return CG_OK;
+  // phi1_rho in the resident row-major layout [NO][n1][LDS]
+  const int n1 = p->n1, lds = res_lds(n1 / 4);
+  std::vector<double> h((size_t)p->NO * n1 * lds, 0.0);
+  for (int c = 0; c < p->NO; ++c)
+    for (int r = 0; r < n1; ++r)
+      for (int q = 0; q < n1; ++q) h[((size_t)c * n1 + r) * lds + q] = d->phi1_rho[((size_t)c * n1 + r) * n1 + q];
+  double* dev_op = nullptr;
+  int rc = upload(p, h.data(), h.size(), &dev_op);
+  if (rc) return rc;
+  p->cluster_rop = dev_op;
+  rc = launch_cluster_steps(p, nullptr, 0, 0, nullptr, nullptr, true);
+  if (rc == CG_EUNSUPPORTED) return CG_OK;  // not schedulable here: keep the two-kernel step
+  if (rc) return rc;
+  p->cluster_step = true;
   return CG_OK;
 }
 
@@ -1412,6 +1517,7 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
   }
   if ((rc = build_stages(p, d))) return bail(rc);
   if ((rc = setup_fused_front(p))) return bail(rc);
+  if ((rc = setup_cluster_step(p, d))) return bail(rc);
   for (const Stage& st : p->stages) {
     if (st.var == VAR_THETA) continue;
     if (st.res_nb) {
@@ -1874,6 +1980,14 @@ static int coupled_steps(cg_coupling* c, cg_plan* bulk, cg_plan* surf, double* W
 namespace {
 
 int run_steps(cg_plan* p, double* state, long long step0, long long nsteps, int* first_bad, cudaStream_t s) {
+  if (p->cluster_step) {
+    // all steps in one kernel, the state resident in the cluster's shared memory
+    int crc = launch_cluster_steps(p, state, step0, nsteps, first_bad, s);
+    if (crc) return crc;
+    set_step_kernel<<<1, 1, 0, s>>>(p->step_dev, (int)(step0 + nsteps));
+    CUDA_TRY(cudaGetLastError());
+    return CG_OK;
+  }
   set_step_kernel<<<1, 1, 0, s>>>(p->step_dev, (int)step0);
   CUDA_TRY(cudaGetLastError());
   int rc;

@@ -49,6 +49,10 @@ struct ThetaParams {
   double tau, limit;
   int* first_bad;
   const int* step;
+  // cluster step kernel (cluster_disk.cuh): shared-space address of the
+  // [2][N/2][8] column slab every CTA of the cluster holds at the same offset
+  unsigned cl_slab;
+  unsigned cl_bar;  // shared-space address of the mbarrier counting the slab's bytes (same offset in every CTA)
 };
 
 // dynamic shared memory: two [W][M+1] complex ping-pong buffers + N twiddles
@@ -483,7 +487,11 @@ __device__ __forceinline__ double2 shfl_d2(double2 v, int src) {
 // BCM: 1 = lines are contiguous rows (Bc == 1), 2 = lines are columns
 // (Bc > 1), 0 = decided at run time.  A compile-time layout keeps the layout
 // branch out of the store loop, so its W loads are batched ahead of the stores.
-template <int M1, int M2, bool AXPY, bool TS = false, bool RS = false, int BCM = 0>
+// CLS (cluster step kernel): a line's results are pushed over DSMEM into the
+// column slabs of the CTAs that own the columns -- base = line * N with lines
+// ordered [species][4 rows of cluster rank r], column pair 2k goes to CTA k / 4
+// at [species][rho row][2k % 8].
+template <int M1, int M2, bool AXPY, bool TS = false, bool RS = false, int BCM = 0, bool CLS = false>
 __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int lt, const double* ph,
                                            const double2* tw, int f, long long base, long long es, int Bc,
                                            const double2* twa = nullptr) {
@@ -684,7 +692,19 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
           y1 = __dadd_rn(wv.y, __dmul_rn(p.tau, y1));
           bad |= !(fabs(y0) <= p.limit) || !(fabs(y1) <= p.limit);
         }
-        *reinterpret_cast<double2*>(p.Y + o) = make_double2(y0, y1);
+        if constexpr (CLS) {
+          constexpr int N = 2 * M, N1 = M, R = 4;
+          const int line = (int)(base / N);
+          const int c = line / R, rho = (int)cluster_ctarank() * R + (line - c * R);
+          const uint32_t dst = mapa_shared(p.cl_slab + (uint32_t)(((c * N1 + rho) * 8 + ((2 * k) & 7)) * 8),
+                                           (uint32_t)(k >> 2));
+          const uint32_t bar = mapa_shared(p.cl_bar, (uint32_t)(k >> 2));
+          asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(dst),
+                       "d"(y0), "d"(y1), "r"(bar)
+                       : "memory");
+        } else {
+          *reinterpret_cast<double2*>(p.Y + o) = make_double2(y0, y1);
+        }
       } else {
         const long long o0 = base + (2LL * k) * es, o1 = o0 + es;
         if (AXPY) {
