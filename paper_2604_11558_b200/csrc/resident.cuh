@@ -64,6 +64,7 @@ struct ResParams {
 constexpr int kResWarps = 16;  // one CTA per SM, four warps per sub-partition
 constexpr int kResParts = 2;   // warps per strip
 constexpr int kResGroups = kResWarps / kResParts;
+constexpr int kResTailMax = 2;  // last rounds of at most this many strips run one block per warp
 
 // shared-memory row stride of the operator copy: >= 4 KSTEPS and 4 (mod 16)
 __host__ __device__ constexpr int res_lds(int ksteps) {
@@ -99,11 +100,13 @@ __device__ __forceinline__ void res_product(const double* o, int j0, int g, int 
 
 // One strip part: blocks [j0, j0 + NL) of the operator extent for strip
 // `strip` of (field f, slab s).  ops / ops2: the resident operator copies (ops2:
-// the chain's second operator); tile_base: the group's exchange tile (CHAIN).
+// the chain's second operator); tile_base: the strip's exchange tile and
+// (bar_id, bar_threads) the named barrier of the warps sharing it (CHAIN).
 template <int VAR, int EPI, int NL, int NBH, int KSTEPS>
 __device__ __forceinline__ void res_strip_part(const ResParams& p, const double* ops, const double* ops2,
-                                               double* tile_base, int grp, int j0, int f, int s, int strip, int lane,
-                                               int step_now) {
+                                               double* tile_base, int bar_id, int bar_threads, int j0, int f, int s,
+                                               int strip, int lane, int step_now, uint64_t* op2_bar = nullptr,
+                                               uint32_t op2_phase = 0) {
   constexpr int LDS = res_lds(KSTEPS);
   const int g = lane >> 2, t = lane & 3;
   const int c = f % p.ncomp;
@@ -148,11 +151,12 @@ __device__ __forceinline__ void res_strip_part(const ResParams& p, const double*
       if (n < 4 * KSTEPS) *reinterpret_cast<double2*>(tile + n) = make_double2(v0, v1);
       acc[j][0] = acc[j][1] = 0.0;
     }
-    named_bar(1 + grp, kResParts * 32);  // both halves of T are written
+    named_bar(bar_id, bar_threads);  // every part of T is written
     double a2[KSTEPS];
 #pragma unroll
     for (int ks = 0; ks < KSTEPS; ++ks) a2[ks] = tile[4 * ks + t];
-    named_bar(1 + grp, kResParts * 32);  // both warps hold T: the tile may be rewritten
+    named_bar(bar_id, bar_threads);  // every warp of the strip holds T: the tile may be rewritten
+    if (op2_bar) mbar_wait(op2_bar, op2_phase);  // first strip after an operator load: the second operator is in
     res_product<VAR, NL, NBH, KSTEPS>(ops2, j0, g, t, a2, acc);
     if (row < p.M) {
       double* orow = p.out + obase + (long long)row * p.ldr;
@@ -244,6 +248,7 @@ __global__ void __launch_bounds__(kResWarps * 32, 1) resident_gemm_kernel(const 
 
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);  // CHAIN: the second operator lands while the first product runs
     fence_barrier_init();
   }
   __syncthreads();
@@ -268,11 +273,13 @@ __global__ void __launch_bounds__(kResWarps * 32, 1) resident_gemm_kernel(const 
         __syncthreads();
       }
       if (threadIdx.x == 0) {
-        mbar_arrive_expect_tx(bar, (uint32_t)(NOPS * OPE * sizeof(double)));
+        mbar_arrive_expect_tx(bar, (uint32_t)(OPE * sizeof(double)));
         bulk_load_1d(base, p.op + (size_t)c * OPE, (uint32_t)(OPE * sizeof(double)), bar);
-        if (NOPS == 2)
+        if (NOPS == 2) {
+          mbar_arrive_expect_tx(bar + 1, (uint32_t)(OPE * sizeof(double)));
           bulk_load_1d(base + (size_t)OPE * sizeof(double), p.op2 + (size_t)c * OPE,
-                       (uint32_t)(OPE * sizeof(double)), bar);
+                       (uint32_t)(OPE * sizeof(double)), bar + 1);
+        }
       }
       loaded = c;
       pending = true;
@@ -282,22 +289,49 @@ __global__ void __launch_bounds__(kResWarps * 32, 1) resident_gemm_kernel(const 
         first = false;
       }
     }
+    uint64_t* bar2 = nullptr;  // CHAIN: waited for between the two products of the segment's first strip
+    uint32_t phase2 = 0;
     if (pending) {
       mbar_wait(bar, phase);
+      if (NOPS == 2) {
+        bar2 = bar + 1;
+        phase2 = phase;
+      }
       phase ^= 1;
       pending = false;
     }
-    // the strip's two warps walk the same strips (the chained pair meets at named barriers)
-    for (long long mine = u + grp; mine < seg_end; mine += kResGroups) {
+    // Full rounds: the strip's two warps walk the same strips (the chained pair
+    // meets at named barriers).  A last round of only one or two strips would
+    // leave them to one or two warp pairs running alone at the dependent-DMMA
+    // rate (n = 100: 17 strips per CTA, the 17th cost 4 us of the chained
+    // kernel's 35): such strips are spread over the whole CTA instead, one 8x8
+    // output block per warp (NB <= 16 warps share the strip's exchange tile).
+    const long long count = seg_end - u;
+    const int tail = (int)(count % kResGroups);
+    const long long round_end = tail > 0 && tail <= kResTailMax ? seg_end - tail : seg_end;
+    for (long long mine = u + grp; mine < round_end; mine += kResGroups) {
       const long long item = mine / p.upi;
       const int strip = (int)(mine - item * p.upi);
       const int f = (int)(item / p.nslab), s = (int)(item - (long long)f * p.nslab);
       if (part == 0)
-        res_strip_part<VAR, EPI, NBH, NBH, KSTEPS>(p, ops, ops + OPE, xch + (size_t)grp * 8 * LDS, grp, 0, f, s, strip,
-                                                   lane, step_now);
+        res_strip_part<VAR, EPI, NBH, NBH, KSTEPS>(p, ops, ops + OPE, xch + (size_t)grp * 8 * LDS, 1 + grp,
+                                                   kResParts * 32, 0, f, s, strip, lane, step_now, bar2, phase2);
       else
-        res_strip_part<VAR, EPI, NBL, NBH, KSTEPS>(p, ops, ops + OPE, xch + (size_t)grp * 8 * LDS, grp, NBH, f, s,
-                                                   strip, lane, step_now);
+        res_strip_part<VAR, EPI, NBL, NBH, KSTEPS>(p, ops, ops + OPE, xch + (size_t)grp * 8 * LDS, 1 + grp,
+                                                   kResParts * 32, NBH, f, s, strip, lane, step_now, bar2, phase2);
+    }
+    if (round_end < seg_end) {
+      // the pairs' tiles are free once every pair is through its last strip
+      if (EPI == EPI_CHAIN) __syncthreads();
+      for (long long mine = round_end; mine < seg_end; ++mine) {
+        const long long item = mine / p.upi;
+        const int strip = (int)(mine - item * p.upi);
+        const int f = (int)(item / p.nslab), s = (int)(item - (long long)f * p.nslab);
+        if (warp < NB)
+          res_strip_part<VAR, EPI, 1, NBH, KSTEPS>(p, ops, ops + OPE, xch, 1 + kResGroups, NB * 32, warp, f, s, strip,
+                                                   lane, step_now, bar2, phase2);
+      }
+      if (EPI == EPI_CHAIN) __syncthreads();  // before a later segment's pairs reuse tile 0
     }
     u = seg_end;
   }
