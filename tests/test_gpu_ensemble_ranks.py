@@ -132,3 +132,14 @@ def test_setup_error_in_one_shard_is_raised_by_every_rank():
     got = _run("gloo", "badsetup")
     assert got[0][0] == "error" and "rank 1" in got[0][1]
     assert got[1][0] == "error" and "NotImplementedError" in got[1][1]
+
+
+def test_single_rank_nccl_group_takes_the_collective_path():
+    """The pool leases one GPU, so the NCCL code path (device-side `agree`
+    all-reduce, `gather_fields` over NCCL) is exercised with a world of one:
+    same result as the run without a process group, bitwise."""
+    got = _run("nccl", "plain", world=1)
+    ref = _single("plain")
+    assert got[0][0] == "ok" and (got[0][3], got[0][4]) == (0, len(MEMBERS))
+    assert np.array_equal(got[0][1], ref.fields)
+    assert np.array_equal(got[0][2], ref.first_bad)
