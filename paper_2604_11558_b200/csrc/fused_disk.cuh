@@ -210,16 +210,43 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
     const double* Wc = Wst + (size_t)comp * (RPB + 2) * N;             // this species' staged rows
     const double* Wo = Wst + (size_t)(1 - comp) * (RPB + 2) * N;       // the other species'
     const double* rowc = Wc + (rr + 1) * N;
-    // F at the point pair (2kk, 2kk+1) of this thread's line (disk_fpair)
-    DiskLine dl;
-    dl.rowc = rowc;
-    dl.rowo = Wo + (rr + 1) * N;
-    dl.rc = rc;
-    dl.kc = kc;
-    dl.lift0 = lift0;
-    dl.lift1 = lift1;
+    // (this kernel keeps its own copy of disk_fpair's arithmetic as a lambda over
+    // the item's locals: routing it through the DiskLine struct cost 4 % here,
+    // 156.2 -> 162.3 us at config 5, profiles/r02_front_variants.txt)
+    // F at the point pair (2kk, 2kk+1): one 16-byte load each for the row,
+    // the rows above and below and the other species, plus the two outer
+    // theta neighbours; same arithmetic as diffusion_rows<0> + the F-build
+    // reaction, so the values equal fbuild_rows_kernel's bit for bit.
     auto fpair = [&](auto compc, int kk) -> double2 {
-      return disk_fpair<KIN, decltype(compc)::value, N>(dl, kin, kk);
+      constexpr int CMP = decltype(compc)::value;  // species, compile-time: the other reaction term is dead code
+      const int x = 2 * kk;
+      const double2 c2 = *reinterpret_cast<const double2*>(rowc + x);
+      const double2 m2 = *reinterpret_cast<const double2*>(rowc - N + x);
+      const double2 p2 = *reinterpret_cast<const double2*>(rowc + N + x);
+      const double2 o2 = *reinterpret_cast<const double2*>(Wo + (rr + 1) * N + x);
+      const double xl = rowc[x == 0 ? N - 1 : x - 1];
+      const double xr = rowc[x + 2 == N ? 0 : x + 2];
+      double2 out;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double x0 = h ? c2.y : c2.x, xm = h ? m2.y : m2.x, xp = h ? p2.y : p2.x;
+        const double left = h ? c2.x : xl, right = h ? xr : c2.y;
+        const double rrv = rc.a * x0 + rc.c * xm + rc.b * xp;
+        const double q = kc.th_off * left + kc.th_diag * x0 + kc.th_off * right;
+        const double d = kc.coeff * (rrv + rc.d * q);
+        double u = CMP == 0 ? x0 : (h ? o2.y : o2.x);
+        double v = CMP == 0 ? (h ? o2.y : o2.x) : x0;
+        if (lift0 != 0.0) u = __dadd_rn(u, lift0);
+        if (lift1 != 0.0) v = __dadd_rn(v, lift1);
+        double g0, g1;
+        reaction<KIN>(kin, u, v, g0, g1);
+        const double val = __dadd_rn(d, CMP == 0 ? g0 : g1);
+        if (h)
+          out.y = val;
+        else
+          out.x = val;
+      }
+      return out;
     };
     // ---- F on the fly, in forward phase A order (columns n2 = lt, lt + TPL, ...)
     double2 keepa[M2 / TPL][M1];
