@@ -240,6 +240,21 @@ int cg_coupled_kinetics(cg_coupling* c, const double* Wb, const double* Ws, doub
 int cg_coupled_run(cg_coupling* c, cg_plan* bulk, cg_plan* surf, double* Wb, double* Ws, long long step0,
                    long long nsteps, int* first_bad, void* stream);
 
+/* ---- standalone mu-mode product and Hadamard product ----
+ * cg_product_*  replace tensor.mode_product(mu, L, field)   tensor.py:31-49
+ *   (np.tensordot + moveaxis: one DGEMM over the matching unfolding): the
+ *   batched DMMA GEMM of the step kernels on one field, the unfolding folded
+ *   into the tensor maps.  dims: the field's extents in C order (ndim 2 or 3,
+ *   the last one even), mu 1-based, L a HOST row-major n_mu x n_mu matrix
+ *   (copied).  apply: T and out are device pointers (16-byte aligned, out of
+ *   place); stream-ordered.
+ * cg_hadamard   replaces tensor.hadamard(A, B)               tensor.py:77-83 */
+typedef struct cg_product cg_product;
+int cg_product_create(int mu, int ndim, const int* dims, const double* L, cg_product** out);
+int cg_product_apply(cg_product* h, const double* T, double* out, void* stream);
+void cg_product_destroy(cg_product* h);
+int cg_hadamard(const double* a, const double* b, double* out, long long n, void* stream);
+
 /* ---- on-device setup ----
  * Batched device replacements for the per-operator host work of prepare()
  * (integrators.py:130-173), for ensembles whose runs do not share operators.

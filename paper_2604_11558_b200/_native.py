@@ -89,6 +89,10 @@ EXPORTS = (
     "cg_coupled_run",
     "cg_weighted_sums_scratch",
     "cg_weighted_sums",
+    "cg_product_create",
+    "cg_product_apply",
+    "cg_product_destroy",
+    "cg_hadamard",
     "cg_setup_eig_tridiag",
     "cg_setup_phi1_matrix",
     "cg_setup_phi1_outer",
@@ -183,6 +187,14 @@ def lib():
                                    ctypes.c_longlong, vp]
     L.cg_weighted_sums.restype = ctypes.c_int
     ci = ctypes.c_int
+    L.cg_product_create.argtypes = [ci, ci, ctypes.POINTER(ci), dp, ctypes.POINTER(vp)]
+    L.cg_product_create.restype = ci
+    L.cg_product_apply.argtypes = [vp, vp, vp, vp]
+    L.cg_product_apply.restype = ci
+    L.cg_product_destroy.argtypes = [vp]
+    L.cg_product_destroy.restype = None
+    L.cg_hadamard.argtypes = [vp, vp, vp, ctypes.c_longlong, vp]
+    L.cg_hadamard.restype = ci
     L.cg_setup_eig_tridiag.argtypes = [ci, ci, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.cg_setup_eig_tridiag.restype = ci
     L.cg_setup_phi1_matrix.argtypes = [ci, ci, vp, vp, vp, vp, vp, vp, vp]

@@ -277,6 +277,12 @@ int launch_gemm(int var, int epi, int cfg, const Maps& m, const GemmParams& p, c
 
 __global__ void set_step_kernel(int* step, int value) { *step = value; }
 
+__global__ void hadamard_kernel(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out,
+                                long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = a[i] * b[i];
+}
+
 // rows of nl values from row stride lds to row stride ldd (padded <-> caller layout)
 __global__ void repack_kernel(const double* __restrict__ src, int lds, double* __restrict__ dst, int ldd,
                               long long rows, int nl) {
@@ -1734,6 +1740,91 @@ int cg_plan_set_step(cg_plan* p, long long step, void* stream) {
   if (!p) return fail(CG_EINVAL, "null plan");
   if (step < 0 || step > INT_MAX) return fail(CG_EINVAL, "step out of range");
   set_step_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(p->step_dev, (int)step);
+  CUDA_TRY(cudaGetLastError());
+  return CG_OK;
+}
+
+// ---- standalone mu-mode product (tensor.mode_product, tensor.py:31-49) ----
+// One GEMM stage of the plan machinery on its own: the field is the stage's
+// source, the caller's output its destination.
+struct cg_product {
+  cg_plan* plan;
+};
+
+int cg_product_create(int mu, int ndim, const int* dims, const double* L, cg_product** out) {
+  if (!dims || !L || !out) return fail(CG_EINVAL, "null argument");
+  *out = nullptr;
+  if (ndim < 2 || ndim > 3) return fail(CG_EINVAL, "fields of order 2 or 3");
+  if (mu < 1 || mu > ndim) return fail(CG_EINVAL, "mode out of range for the field's order");
+  for (int i = 0; i < ndim; ++i)
+    if (dims[i] < 1) return fail(CG_EINVAL, "extents must be positive");
+  if (dims[ndim - 1] % 2 != 0) return fail(CG_EUNSUPPORTED, "the contiguous (last) extent must be even");
+  cg_plan* p = new cg_plan();
+  p->geom = ndim == 3 ? CG_CYLINDER : CG_DISK;  // only names the order of the field here
+  p->n1 = dims[0];
+  p->n2 = dims[1];
+  p->n3 = ndim == 3 ? dims[2] : 1;
+  p->B = p->C = p->NO = 1;
+  p->kin = CG_KIN_EXTERNAL;
+  p->P = 0;
+  p->tau = 0.0;
+  p->nl = dims[ndim - 1];
+  p->ld = p->nl;
+  p->padded = false;
+  p->npts = p->npts_u = (long long)p->n1 * p->n2 * p->n3;
+  p->elems = p->elems_u = p->npts;
+  const int n = dims[mu - 1];
+  auto get = [&](int, int r, int q) { return L[(size_t)r * n + q]; };
+  int rc;
+  if (mu == ndim)  // last mode: Y = X L^T over contiguous rows
+    rc = add_stage(p, VAR_TN, EPI_STORE, (int)(p->npts / n), n, n, 1, BUF_X, BUF_OUT, n, get);
+  else if (mu == 1)  // first mode: Y = L X over the flattened trailing extents
+    rc = add_stage(p, VAR_NN, EPI_STORE, n, (int)(p->npts / n), n, 1, BUF_X, BUF_OUT, n, get);
+  else  // middle mode of an order-3 field: one slab per leading index
+    rc = add_stage(p, VAR_NN, EPI_STORE, n, p->n3, n, p->n1, BUF_X, BUF_OUT, n, get);
+  if (rc == CG_OK) {
+    const Stage& st = p->stages[0];
+    if (st.res_nb) {
+      ResParams rp{};
+      rc = launch_resident(st.var, st.epi, st.res_nb, rp, nullptr, true);
+    } else {
+      Maps dummy{};
+      GemmParams gp{};
+      rc = launch_gemm(st.var, st.epi, st.cfg, dummy, gp, nullptr, true);
+    }
+  }
+  if (rc == CG_OK && cudaDeviceSynchronize() != cudaSuccess) rc = fail(CG_ECUDA, "operator upload failed");
+  if (rc) {
+    cg_plan_destroy(p);
+    return rc;
+  }
+  *out = new cg_product{p};
+  return CG_OK;
+}
+
+int cg_product_apply(cg_product* h, const double* T, double* out, void* stream) {
+  if (!h || !T || !out) return fail(CG_EINVAL, "null argument");
+  if (T == out) return fail(CG_EINVAL, "mode products are out of place");
+  if ((reinterpret_cast<uintptr_t>(T) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(CG_EINVAL, "fields must be 16-byte aligned");
+  cg_plan* p = h->plan;
+  p->X = const_cast<double*>(T);  // the stage's source buffer (read only)
+  return launch_stage(p, p->stages[0], nullptr, out, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+void cg_product_destroy(cg_product* h) {
+  if (!h) return;
+  h->plan->X = nullptr;
+  cg_plan_destroy(h->plan);
+  delete h;
+}
+
+// hadamard(A, B) (tensor.py:77-83): out = a * b elementwise
+int cg_hadamard(const double* a, const double* b, double* out, long long n, void* stream) {
+  if (!a || !b || !out) return fail(CG_EINVAL, "null argument");
+  if (n < 1) return fail(CG_EINVAL, "n must be positive");
+  const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148LL * 16);
+  hadamard_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, b, out, n);
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
 }
