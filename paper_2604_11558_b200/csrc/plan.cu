@@ -1474,6 +1474,10 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
   p->npts = p->npts_u / p->nl * p->ld;
   p->elems = p->npts * p->B * p->C;
   p->elems_u = p->npts_u * p->B * p->C;
+  if (p->npts >= (1LL << 31)) {  // kernels index within a field with 32-bit offsets
+    delete p;
+    return fail(CG_EUNSUPPORTED, "a field of 2^31 or more points is not supported");
+  }
   if (d->ops_per_run != 0 && d->ops_per_run != 1) return fail(CG_EINVAL, "ops_per_run must be 0 or 1");
   p->NO = d->ops_per_run ? p->B * p->C : p->C;
   {

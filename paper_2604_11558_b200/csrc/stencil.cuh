@@ -143,8 +143,11 @@ struct FbuildShape {
 // 3-D: X points at column j0; centre block jj at rows jj (RB + 2) ..., the
 // theta halo (columns j0 - 1 and j0 + jn, periodic) at JB (RB + 2) + [0, 2 RB)
 template <int GEOM>
+// (offsets within one field are 32-bit: a field holds < 2^31 elements, checked
+// at plan creation; 64-bit index arithmetic per load made the 3-D kernels
+// issue-bound)
 __device__ __forceinline__ void stage_rows(double* s, const double* __restrict__ X, int i0, int j, int n1, int n2,
-                                           int nl, long long rs, int jst) {
+                                           int nl, int rs, int jst) {
   using S = FbuildShape<GEOM>;
   const bool periodic_walk = (GEOM == 1);
   const int l = threadIdx.x;
@@ -152,13 +155,13 @@ __device__ __forceinline__ void stage_rows(double* s, const double* __restrict__
   const int jn = S::D3 ? min(S::JB, n2 - j) : 1;  // valid columns of this CTA
 #pragma unroll
   for (int jj = 0; jj < S::JB; ++jj) {
-    const long long jo = (long long)(jj < jn ? jj : jn - 1) * jst;
+    const int jo = (jj < jn ? jj : jn - 1) * jst;
 #pragma unroll
     for (int r = 0; r < S::RB + 2; ++r) {
       int i = i0 - 1 + r;
       if (i < 0) i = periodic_walk ? n1 - 1 : 0;
       if (i >= n1) i = periodic_walk ? i - n1 : n1 - 1;
-      s[(jj * (S::RB + 2) + r) * nl + l] = __ldg(X + (long long)i * rs + jo + l);
+      s[(jj * (S::RB + 2) + r) * nl + l] = __ldg(X + (i * rs + jo + l));
     }
   }
   if (S::D3) {
@@ -168,8 +171,8 @@ __device__ __forceinline__ void stage_rows(double* s, const double* __restrict__
 #pragma unroll
     for (int r = 0; r < S::RB; ++r) {
       const int i = min(i0 + r, n1 - 1);
-      s[(H + r) * nl + l] = __ldg(X + (long long)i * rs + (long long)(jm - j) * jst + l);
-      s[(H + S::RB + r) * nl + l] = __ldg(X + (long long)i * rs + (long long)(jp - j) * jst + l);
+      s[(H + r) * nl + l] = __ldg(X + (i * rs + (jm - j) * jst + l));
+      s[(H + S::RB + r) * nl + l] = __ldg(X + (i * rs + (jp - j) * jst + l));
     }
   }
 }
@@ -282,8 +285,8 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
   const int j = S::D3 ? (int)blockIdx.y * S::JB : 0;  // first theta column
   const int jn = S::D3 ? min(S::JB, p.n2 - j) : 1;
   const int b = blockIdx.z;
-  const long long rsw = S::D3 ? (long long)p.n2 * p.ldw : (long long)p.ldw;
-  const long long rsf = S::D3 ? (long long)p.n2 * p.ldf : (long long)p.ldf;
+  const int rsw = S::D3 ? p.n2 * p.ldw : p.ldw;
+  const int rsf = S::D3 ? p.n2 * p.ldf : p.ldf;
   const long long wbase = (long long)b * p.ncomp * p.npw + (long long)j * (S::D3 ? p.ldw : 0);
   const long long fbase = (long long)b * p.ncomp * p.npf + (long long)j * (S::D3 ? p.ldf : 0);
   const int plane = S::ROWS * nl;
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
           for (int r = 0; r < S::RB; ++r) {
             const int i = i0 + r;
             if (i >= n1) break;
-            const long long idx = fbase + (long long)jj * p.ldf + (long long)c * p.npf + (long long)i * rsf + l;
+            const long long idx = fbase + (long long)c * p.npf + (jj * p.ldf + i * rsf + l);
             double val = 0.0;
             if (p.with_diffusion)
               val = k.coeff * diffusion_rows<GEOM>(k, rcs[(c < 8 ? c : 7) * S::RB + r], fb_smem, r, l, nl, jj, jn);
@@ -331,13 +334,14 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
     const bool with_r = p.with_reaction;
     __syncthreads();
     if (l >= nl) return;
-    double* __restrict__ Fo = p.F;
+    double* __restrict__ Fo = p.F + fbase;       // species 0 of this CTA's run / theta column
+    double* __restrict__ Fo1 = Fo + p.npf;       // species 1
     for (int jj = 0; jj < jn; ++jj) {
 #pragma unroll
     for (int r = 0; r < S::RB; ++r) {
       const int i = i0 + r;
       if (i >= n1) break;
-      const long long off = fbase + (long long)jj * p.ldf + (long long)i * rsf + l;
+      const int off = jj * p.ldf + i * rsf + l;
       const int cs = (jj * (S::RB + 2) + r + 1) * nl + l;  // centre value in the stage
       double g0 = 0.0, g1 = 0.0;
       if (with_r) {
@@ -354,7 +358,7 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
         fv = with_r ? __dadd_rn(dv, g1) : dv;
       }
       Fo[off] = fu;
-      Fo[off + p.npf] = fv;
+      Fo1[off] = fv;
     }
     }
   }
