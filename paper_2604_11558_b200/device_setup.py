@@ -33,6 +33,9 @@ from .operators import EigenFactorization, NumericalFailure, eig_theta
 from .phifun import PhiTensor
 
 
+_MAX_SETS = 32768  # sets per cg_setup_phi1_* launch (the C ABI takes up to 65535)
+
+
 def _stream():
     import torch
 
@@ -120,9 +123,12 @@ def _phi1_matrices(batch: _EigBatch, mats, scales):
     out = torch.empty((nset, n, n), dtype=torch.float64, device="cuda")
     mat = torch.tensor(mats, dtype=torch.int32, device="cuda")
     s = _dev(scales)
-    _native.check(_native.lib().cg_setup_phi1_matrix(nset, n, batch.lam.data_ptr(), batch.Qt.data_ptr(),
-                                                     batch.xi.data_ptr(), mat.data_ptr(), s.data_ptr(),
-                                                     out.data_ptr(), _stream()), "cg_setup_phi1_matrix")
+    for lo in range(0, nset, _MAX_SETS):  # one launch takes at most 65535 sets (grid z extent)
+        hi = min(nset, lo + _MAX_SETS)
+        _native.check(_native.lib().cg_setup_phi1_matrix(hi - lo, n, batch.lam.data_ptr(), batch.Qt.data_ptr(),
+                                                         batch.xi.data_ptr(), mat[lo:hi].data_ptr(),
+                                                         s[lo:hi].data_ptr(), out[lo:hi].data_ptr(), _stream()),
+                      "cg_setup_phi1_matrix")
     return out
 
 
@@ -136,9 +142,14 @@ def _phi1_outer(f1, f2, f3, scales):
     shape = (nset, n1, n2) if f3 is None else (nset, n1, n2, n3)
     out = torch.empty(shape, dtype=torch.float64, device="cuda")
     s = _dev(scales)
-    _native.check(_native.lib().cg_setup_phi1_outer(nset, n1, n2, n3, f1.data_ptr(), f2.data_ptr(),
-                                                    None if f3 is None else f3.data_ptr(), s.data_ptr(),
-                                                    out.data_ptr(), _stream()), "cg_setup_phi1_outer")
+    f1, f2 = f1.contiguous(), f2.contiguous()
+    f3 = None if f3 is None else f3.contiguous()
+    for lo in range(0, nset, _MAX_SETS):
+        hi = min(nset, lo + _MAX_SETS)
+        _native.check(_native.lib().cg_setup_phi1_outer(hi - lo, n1, n2, n3, f1[lo:hi].data_ptr(), f2[lo:hi].data_ptr(),
+                                                        None if f3 is None else f3[lo:hi].data_ptr(),
+                                                        s[lo:hi].data_ptr(), out[lo:hi].data_ptr(), _stream()),
+                      "cg_setup_phi1_outer")
     return out
 
 
