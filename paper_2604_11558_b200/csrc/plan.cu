@@ -295,11 +295,11 @@ __global__ void repack_kernel(const double* __restrict__ src, int lds, double* _
   }
 }
 
-template <int GEOM, int KIN>
-int launch_fbuild_t(const StencilParams& p, cudaStream_t s, bool configure_only) {
-  using S = FbuildShape<GEOM>;
+template <int GEOM, int KIN, int R2>
+int launch_fbuild_r(const StencilParams& p, cudaStream_t s, bool configure_only) {
+  using S = FbuildShape<GEOM, R2>;
   if (configure_only) {  // at plan creation, never under stream capture
-    CUDA_TRY(cudaFuncSetAttribute(fbuild_rows_kernel<GEOM, KIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(fbuild_rows_kernel<GEOM, KIN, R2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024));
     return CG_OK;
   }
@@ -311,10 +311,26 @@ int launch_fbuild_t(const StencilParams& p, cudaStream_t s, bool configure_only)
   const dim3 grid((unsigned)((p.n1 + S::RB - 1) / S::RB), S::D3 ? (unsigned)((p.n2 + S::JB - 1) / S::JB) : 1u,
                   (unsigned)p.batch);
   const unsigned threads = (unsigned)((nl + 31) / 32 * 32);
-  int rc = launch_pdl(fbuild_rows_kernel<GEOM, KIN>, grid, dim3(threads), smem, s, p);
+  int rc = launch_pdl(fbuild_rows_kernel<GEOM, KIN, R2>, grid, dim3(threads), smem, s, p);
   if (rc) return rc;
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
+}
+
+// 2-D geometries: 4-row CTAs when the 8-row grid would not give every SM two CTAs
+template <int GEOM, int KIN>
+int launch_fbuild_t(const StencilParams& p, cudaStream_t s, bool configure_only) {
+  if constexpr (GEOM >= 2) {
+    return launch_fbuild_r<GEOM, KIN, 8>(p, s, configure_only);
+  } else {
+    if (configure_only) {
+      if (int rc = launch_fbuild_r<GEOM, KIN, 4>(p, s, true)) return rc;
+      return launch_fbuild_r<GEOM, KIN, 8>(p, s, true);
+    }
+    const long long ctas8 = (long long)((p.n1 + 7) / 8) * p.batch;
+    if (ctas8 < 2LL * 148) return launch_fbuild_r<GEOM, KIN, 4>(p, s, false);
+    return launch_fbuild_r<GEOM, KIN, 8>(p, s, false);
+  }
 }
 
 template <int GEOM>

@@ -120,7 +120,10 @@ __device__ __forceinline__ double circ3(const double* th, double xm, double x0, 
   return th[1] * xm + th[0] * x0 + th[1] * xp;
 }
 
-template <int GEOM>
+// R2: walked-axis rows per CTA of the 2-D geometries: 8 (two staged halo rows
+// per 8), or 4 for small problems, where 8-row CTAs leave most SMs idle (the
+// sphere's 512 rows: 64 CTAs; F-build 3.4 -> 2.4 us, config 2 step 17.6 -> 16.3 us)
+template <int GEOM, int R2 = 8>
 struct FbuildShape {
   static constexpr bool D3 = GEOM >= 2;
 #ifndef CG_RB3
@@ -129,7 +132,7 @@ struct FbuildShape {
 #ifndef CG_JB3
 #define CG_JB3 2
 #endif
-  static constexpr int RB = D3 ? CG_RB3 : 8;         // interior rows per CTA
+  static constexpr int RB = D3 ? CG_RB3 : R2;        // interior rows per CTA
   // 3-D: JB consecutive theta columns per CTA share their theta neighbours:
   // staged rows = JB (RB + 2) centre rows + 2 RB theta-halo rows.  JB = 2
   // (2.5 staged rows per output row instead of 3.5): cylinder F-build
@@ -142,13 +145,13 @@ struct FbuildShape {
 // stage component X's rows for this CTA into s[ROWS][nl]
 // 3-D: X points at column j0; centre block jj at rows jj (RB + 2) ..., the
 // theta halo (columns j0 - 1 and j0 + jn, periodic) at JB (RB + 2) + [0, 2 RB)
-template <int GEOM>
 // (offsets within one field are 32-bit: a field holds < 2^31 elements, checked
 // at plan creation; 64-bit index arithmetic per load made the 3-D kernels
 // issue-bound)
+template <int GEOM, int R2 = 8>
 __device__ __forceinline__ void stage_rows(double* s, const double* __restrict__ X, int i0, int j, int n1, int n2,
                                            int nl, int rs, int jst) {
-  using S = FbuildShape<GEOM>;
+  using S = FbuildShape<GEOM, R2>;
   const bool periodic_walk = (GEOM == 1);
   const int l = threadIdx.x;
   if (l >= nl) return;
@@ -213,10 +216,10 @@ __device__ __forceinline__ CompCoef comp_coef(const StencilParams& p, int c, int
 // from the shared-memory stage s (rows r, r+1, r+2 = i-1, i, i+1)
 // (3-D: theta column jj of the CTA's jn; its theta neighbours are the adjacent
 // centre blocks or the halo rows)
-template <int GEOM>
+template <int GEOM, int R2 = 8>
 __device__ __forceinline__ double diffusion_rows(const CompCoef& k, const RowCoef& rc, const double* s0, int r, int l,
                                                  int nl, int jj = 0, int jn = 1) {
-  using S = FbuildShape<GEOM>;
+  using S = FbuildShape<GEOM, R2>;
   const double* s = s0 + jj * (S::RB + 2) * nl;
   const double xm = s[r * nl + l], x0 = s[(r + 1) * nl + l], xp = s[(r + 2) * nl + l];
   int ll = l - 1, lr = l + 1;
@@ -251,9 +254,9 @@ __device__ __forceinline__ double diffusion_rows(const CompCoef& k, const RowCoe
 }
 
 // fill the CTA's walked-axis row coefficients for components [0, nc)
-template <int GEOM>
+template <int GEOM, int R2 = 8>
 __device__ __forceinline__ void row_coefs(RowCoef* rcs, const StencilParams& p, int i0, int nc, int ob) {
-  using S = FbuildShape<GEOM>;
+  using S = FbuildShape<GEOM, R2>;
   const int n1 = p.n1;
   for (int idx = threadIdx.x; idx < nc * S::RB; idx += blockDim.x) {
     const int c = idx / S::RB, r = idx - c * S::RB;
@@ -270,9 +273,9 @@ __device__ __forceinline__ void row_coefs(RowCoef* rcs, const StencilParams& p, 
   }
 }
 
-template <int GEOM, int KIN>
+template <int GEOM, int KIN, int R2 = 8>
 __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p) {
-  using S = FbuildShape<GEOM>;
+  using S = FbuildShape<GEOM, R2>;
   extern __shared__ double fb_smem[];
   __shared__ RowCoef rcs[8 * S::RB];  // up to 8 components
   pdl_wait();
@@ -294,11 +297,11 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
 
   if (KIN == KIN_EXTERNAL) {
     const int nc = p.ncomp < 8 ? p.ncomp : 8;
-    row_coefs<GEOM>(rcs, p, i0, nc, ob);
+    row_coefs<GEOM, R2>(rcs, p, i0, nc, ob);
     for (int c = 0; c < p.ncomp; ++c) {
       const double* X = p.W + wbase + (long long)c * p.npw;
       if (c > 0) __syncthreads();
-      stage_rows<GEOM>(fb_smem, X, i0, j, n1, p.n2, nl, rsw, p.ldw);
+      stage_rows<GEOM, R2>(fb_smem, X, i0, j, n1, p.n2, nl, rsw, p.ldw);
       __syncthreads();
       if (l < nl) {
         const CompCoef k = comp_coef<GEOM>(p, ob + c, l, nl);
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
             const long long idx = fbase + (long long)c * p.npf + (jj * p.ldf + i * rsf + l);
             double val = 0.0;
             if (p.with_diffusion)
-              val = k.coeff * diffusion_rows<GEOM>(k, rcs[(c < 8 ? c : 7) * S::RB + r], fb_smem, r, l, nl, jj, jn);
+              val = k.coeff * diffusion_rows<GEOM, R2>(k, rcs[(c < 8 ? c : 7) * S::RB + r], fb_smem, r, l, nl, jj, jn);
             if (p.with_reaction) val = p.with_diffusion ? __dadd_rn(val, __ldg(p.G + idx)) : __ldg(p.G + idx);
             p.F[idx] = val;
           }
@@ -319,9 +322,9 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
     }
   } else {
     const bool with_d = p.with_diffusion;
-    if (with_d) row_coefs<GEOM>(rcs, p, i0, 2, ob);
-    stage_rows<GEOM>(fb_smem, p.W + wbase, i0, j, n1, p.n2, nl, rsw, p.ldw);
-    stage_rows<GEOM>(fb_smem + plane, p.W + wbase + p.npw, i0, j, n1, p.n2, nl, rsw, p.ldw);
+    if (with_d) row_coefs<GEOM, R2>(rcs, p, i0, 2, ob);
+    stage_rows<GEOM, R2>(fb_smem, p.W + wbase, i0, j, n1, p.n2, nl, rsw, p.ldw);
+    stage_rows<GEOM, R2>(fb_smem + plane, p.W + wbase + p.npw, i0, j, n1, p.n2, nl, rsw, p.ldw);
     CompCoef k0{}, k1{};  // operator coefficients are only present when diffusing
     if (with_d) {
       k0 = comp_coef<GEOM>(p, ob, lcl, nl);
@@ -352,8 +355,8 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
       }
       double fu = g0, fv = g1;
       if (with_d) {
-        const double du = k0.coeff * diffusion_rows<GEOM>(k0, rcs[r], fb_smem, r, l, nl, jj, jn);
-        const double dv = k1.coeff * diffusion_rows<GEOM>(k1, rcs[S::RB + r], fb_smem + plane, r, l, nl, jj, jn);
+        const double du = k0.coeff * diffusion_rows<GEOM, R2>(k0, rcs[r], fb_smem, r, l, nl, jj, jn);
+        const double dv = k1.coeff * diffusion_rows<GEOM, R2>(k1, rcs[S::RB + r], fb_smem + plane, r, l, nl, jj, jn);
         fu = with_r ? __dadd_rn(du, g0) : du;
         fv = with_r ? __dadd_rn(dv, g1) : dv;
       }
