@@ -78,5 +78,30 @@ def main():
                 plan.close()
 
 
+def cluster_runs():
+    """The cluster step kernel (all steps of cg_run in one launch, DSMEM hand-over
+    on tx-count mbarriers): REPS reruns of 60 steps from the same state."""
+    os.environ.pop("CURVIGPU_TILE_CFG", None)
+    os.environ.pop("CURVIGPU_RESIDENT", None)
+    for dims in ((64, 128), (32, 64)):
+        system = configs.BUILDERS[1](dims)
+        geos = [prepare(c.ops, 1e-3) for c in system.components]
+        plan = SplitPlan(geos, 1, system.kinetics.kind, system.kinetics.param_vector()[None, :], theta="fft")
+        W0 = torch.from_numpy(np.stack([c.initial for c in system.components])[None].copy()).cuda()
+        bad = torch.full((1, 2), 2**31 - 1, dtype=torch.int32, device="cuda")
+        first, ndiff = None, 0
+        for _ in range(REPS):
+            state = W0.clone()
+            plan.run(state, 0, 60, bad)
+            if first is None:
+                first = state.clone()
+            elif not torch.equal(state, first):
+                ndiff += 1
+        print(json.dumps({"config": 1, "dims": list(dims), "kernel": "disk_cluster_kernel", "steps": 60,
+                          "reps": REPS, "runs_differing": ndiff}), flush=True)
+        plan.close()
+
+
 if __name__ == "__main__":
     main()
+    cluster_runs()
