@@ -93,6 +93,13 @@ class ClockSampler:
             out, _ = self.proc.communicate()
         sms, maxes, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sampled = len(out.strip().splitlines())
+        if not sampled:
+            # a timed region shorter than the sampler's start-up: one query right after it
+            try:
+                out = subprocess.run(self.proc.args[:-2], capture_output=True, text=True, timeout=20).stdout
+            except Exception:
+                out = ""
         for line in out.strip().splitlines():
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 7:
@@ -110,7 +117,7 @@ class ClockSampler:
         loaded = [s for s in sms if s > 500] or sms
         loaded.sort()
         return {"sm_mhz": loaded[len(loaded) // 2], "sm_max_mhz": max(maxes), "reasons": sorted(reasons),
-                "samples": len(sms)}
+                "samples": len(sms) if sampled else 0}
 
 
 # ---------------------------------------------------------------------------
