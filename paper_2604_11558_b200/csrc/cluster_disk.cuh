@@ -161,14 +161,16 @@ __global__ void __launch_bounds__(256, 1) disk_cluster_kernel(const ClusterDiskP
   DiskLine dl;
   {
     const int oc = b * sp.opb + fcomp;
-    dl.kc = comp_coef<0>(sp, oc, 0, N);
+    const CompCoef kc = comp_coef<0>(sp, oc, 0, N);
     const double* bands = sp.rho_b + (long long)oc * 3 * N1;
-    dl.rc.a = __ldg(bands + frow);
-    dl.rc.b = (frow < N1 - 1) ? __ldg(bands + N1 + frow) : 0.0;
-    dl.rc.c = (frow > 0) ? __ldg(bands + 2 * N1 + frow - 1) : 0.0;
-    dl.rc.d = __ldg(sp.d_rho + (long long)oc * N1 + frow);
-    dl.lift0 = sp.lift[0];
-    dl.lift1 = sp.lift[1];
+    RowCoef rc;
+    rc.a = __ldg(bands + frow);
+    rc.b = (frow < N1 - 1) ? __ldg(bands + N1 + frow) : 0.0;
+    rc.c = (frow > 0) ? __ldg(bands + 2 * N1 + frow - 1) : 0.0;
+    rc.d = __ldg(sp.d_rho + (long long)oc * N1 + frow);
+    fold_disk_row(rc, kc, dl.fa, dl.fb, dl.fc, dl.fe);
+    dl.lift0 = lift_addend(sp.lift[0]);
+    dl.lift1 = lift_addend(sp.lift[1]);
     dl.rowc = wrows + ((size_t)fcomp * (R + 2) + frr + 1) * N;
     dl.rowo = wrows + ((size_t)(1 - fcomp) * (R + 2) + frr + 1) * N;
   }

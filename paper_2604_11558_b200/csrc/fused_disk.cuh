@@ -33,17 +33,29 @@ constexpr bool kNoRegSplit = false;
 struct DiskLine {
   const double* rowc;
   const double* rowo;
-  RowCoef rc;
-  CompCoef kc;
-  double lift0, lift1;
+  double fa, fb, fc, fe;  // folded stencil row (fold_disk_row)
+  double lift0, lift1;  // lift_addend() values
 };
+
+// The disk's diffusion row coeff * (a x0 + c x- + b x+ + d (off xl + diag x0 +
+// off xr)) with the line's constants folded once per line: five FP64
+// instructions per point instead of eight (the front is issue-bound).  The
+// rounding differs from fbuild_rows_kernel's unfolded form by a few ulp of the
+// largest term, as any reassociation of the reference's dense products does.
+__device__ __forceinline__ void fold_disk_row(const RowCoef& rc, const CompCoef& kc, double& fa, double& fb, double& fc,
+                                              double& fe) {
+  fa = kc.coeff * (rc.a + rc.d * kc.th_diag);
+  fb = kc.coeff * rc.b;
+  fc = kc.coeff * rc.c;
+  fe = kc.coeff * (rc.d * kc.th_off);
+}
 
 // F = coeff * (A_rho W + d_rho (W A_theta)) + g(W + lift) at the point pair
 // (2kk, 2kk+1) of a line: one 16-byte load each for the row, the rows above
-// and below and the other species, plus the two outer theta neighbours; same
-// arithmetic as diffusion_rows<0> + the F-build reaction, so the values equal
-// fbuild_rows_kernel's bit for bit.  CMP: the line's species (compile-time:
-// the other species' reaction term is dead code).
+// and below and the other species, plus the two outer theta neighbours; the
+// folded stencil row above plus the F-build kernel's reaction (bit for bit).
+// CMP: the line's species (compile-time: the other species' reaction term is
+// dead code).
 template <int KIN, int CMP, int N>
 __device__ __forceinline__ double2 disk_fpair(const DiskLine& L, const double (&kin)[9], int kk) {
   const int x = 2 * kk;
@@ -59,13 +71,11 @@ __device__ __forceinline__ double2 disk_fpair(const DiskLine& L, const double (&
   for (int h = 0; h < 2; ++h) {
     const double x0 = h ? c2.y : c2.x, xm = h ? m2.y : m2.x, xp = h ? p2.y : p2.x;
     const double left = h ? c2.x : xl, right = h ? xr : c2.y;
-    const double rrv = L.rc.a * x0 + L.rc.c * xm + L.rc.b * xp;
-    const double q = L.kc.th_off * left + L.kc.th_diag * x0 + L.kc.th_off * right;
-    const double d = L.kc.coeff * (rrv + L.rc.d * q);
+    const double d = L.fa * x0 + L.fc * xm + L.fb * xp + L.fe * (left + right);
     double u = CMP == 0 ? x0 : (h ? o2.y : o2.x);
     double v = CMP == 0 ? (h ? o2.y : o2.x) : x0;
-    if (L.lift0 != 0.0) u = __dadd_rn(u, L.lift0);
-    if (L.lift1 != 0.0) v = __dadd_rn(v, L.lift1);
+    u = __dadd_rn(u, L.lift0);  // lift_addend values: unconditional adds
+    v = __dadd_rn(v, L.lift1);
     double g0, g1;
     reaction<KIN>(kin, u, v, g0, g1);
     const double val = __dadd_rn(d, CMP == 0 ? g0 : g1);
@@ -177,7 +187,7 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
   const int tid = threadIdx.x;
   const int ln = tid / TPL, lt = tid - ln * TPL;
   const int comp = ln / RPB, rr = ln - comp * RPB;  // line = (species, interior row)
-  const double lift0 = sp.lift[0], lift1 = sp.lift[1];
+  const double lift0 = lift_addend(sp.lift[0]), lift1 = lift_addend(sp.lift[1]);
   mbar_wait(&full[2], 0);
   for (int i = threadIdx.x; i < M; i += blockDim.x) twa_s[i] = tw_s[2 * (i % M2) * (i / M2)];
   __syncthreads();
@@ -205,6 +215,8 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
       rc.c = (row > 0) ? __ldg(bands + 2 * n1 + row - 1) : 0.0;
       rc.d = __ldg(sp.d_rho + (long long)oc * n1 + row);
     }
+    double fa, fb, fc, fe;
+    fold_disk_row(rc, kc, fa, fb, fc, fe);
     mbar_wait(&full[k], NBUF == 2 ? ((t >> 1) & 1) : (t & 1));
 
     const double* Wc = Wst + (size_t)comp * (RPB + 2) * N;             // this species' staged rows
@@ -215,8 +227,8 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
     // 156.2 -> 162.3 us at config 5, profiles/r02_front_variants.txt)
     // F at the point pair (2kk, 2kk+1): one 16-byte load each for the row,
     // the rows above and below and the other species, plus the two outer
-    // theta neighbours; same arithmetic as diffusion_rows<0> + the F-build
-    // reaction, so the values equal fbuild_rows_kernel's bit for bit.
+    // theta neighbours; the same arithmetic as disk_fpair, so the cluster step
+    // kernel and this front produce the same F bit for bit.
     auto fpair = [&](auto compc, int kk) -> double2 {
       constexpr int CMP = decltype(compc)::value;  // species, compile-time: the other reaction term is dead code
       const int x = 2 * kk;
@@ -231,13 +243,11 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
       for (int h = 0; h < 2; ++h) {
         const double x0 = h ? c2.y : c2.x, xm = h ? m2.y : m2.x, xp = h ? p2.y : p2.x;
         const double left = h ? c2.x : xl, right = h ? xr : c2.y;
-        const double rrv = rc.a * x0 + rc.c * xm + rc.b * xp;
-        const double q = kc.th_off * left + kc.th_diag * x0 + kc.th_off * right;
-        const double d = kc.coeff * (rrv + rc.d * q);
+        const double d = fa * x0 + fc * xm + fb * xp + fe * (left + right);
         double u = CMP == 0 ? x0 : (h ? o2.y : o2.x);
         double v = CMP == 0 ? (h ? o2.y : o2.x) : x0;
-        if (lift0 != 0.0) u = __dadd_rn(u, lift0);
-        if (lift1 != 0.0) v = __dadd_rn(v, lift1);
+        u = __dadd_rn(u, lift0);
+        v = __dadd_rn(v, lift1);
         double g0, g1;
         reaction<KIN>(kin, u, v, g0, g1);
         const double val = __dadd_rn(d, CMP == 0 ? g0 : g1);

@@ -46,6 +46,13 @@ struct StencilParams {
   int* step;           // incremented once per launch when non-null
 };
 
+// The reference's kinetics closures add a component's lift only in lifted
+// models (models.py:528-532; unlifted models pass the state through).
+// x + (-0.0) == x bit for bit for every x (signed zeros included), so a zero
+// lift becomes the addend -0.0 and the add is unconditional: no per-point
+// select (256 FSEL in the fused disk front).
+__device__ __forceinline__ double lift_addend(double lift) { return lift != 0.0 ? lift : -0.0; }
+
 // Two-species reaction, rounded operation by operation in the reference's
 // NumPy order (no FMA contraction), so g matches the oracle bit for bit.
 template <int KIN>
@@ -333,7 +340,7 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
     double kin[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) kin[q] = (q < p.nparams) ? p.kin[(long long)b * p.nparams + q] : 0.0;
-    const double lift0 = p.lift[0], lift1 = p.lift[1];
+    const double lift0 = lift_addend(p.lift[0]), lift1 = lift_addend(p.lift[1]);
     const bool with_r = p.with_reaction;
     __syncthreads();
     if (l >= nl) return;
@@ -349,8 +356,8 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
       double g0 = 0.0, g1 = 0.0;
       if (with_r) {
         double u = fb_smem[cs], v = fb_smem[plane + cs];
-        if (lift0 != 0.0) u = __dadd_rn(u, lift0);
-        if (lift1 != 0.0) v = __dadd_rn(v, lift1);
+        u = __dadd_rn(u, lift0);
+        v = __dadd_rn(v, lift1);
         reaction<KIN>(kin, u, v, g0, g1);
       }
       double fu = g0, fv = g1;

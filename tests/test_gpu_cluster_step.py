@@ -36,7 +36,7 @@ def test_cluster_steps_equal_the_two_kernel_step(monkeypatch, dims, m):
     cl, two = _both(monkeypatch, lambda: run_simulation(pcfg.BUILDERS[1](dims), m, m * 1e-3).fields)
     for name in two:
         # phase A is the fused front's arithmetic; the rho product groups k in other 4-blocks
-        assert rel_inf(cl[name], two[name]) <= 1e-13 * max(1, m // 10), (dims, m, name)
+        assert rel_inf(cl[name], two[name]) <= 2e-13 * max(1, m // 10), (dims, m, name)
         assert not np.array_equal(cl[name], pcfg.BUILDERS[1](dims).components[0].initial)
 
 
