@@ -71,14 +71,14 @@ __device__ __forceinline__ double2 disk_fpair(const DiskLine& L, const double (&
   for (int h = 0; h < 2; ++h) {
     const double x0 = h ? c2.y : c2.x, xm = h ? m2.y : m2.x, xp = h ? p2.y : p2.x;
     const double left = h ? c2.x : xl, right = h ? xr : c2.y;
-    const double d = L.fa * x0 + L.fc * xm + L.fb * xp + L.fe * (left + right);
     double u = CMP == 0 ? x0 : (h ? o2.y : o2.x);
     double v = CMP == 0 ? (h ? o2.y : o2.x) : x0;
     u = __dadd_rn(u, L.lift0);  // lift_addend values: unconditional adds
     v = __dadd_rn(v, L.lift1);
     double g0, g1;
     reaction<KIN>(kin, u, v, g0, g1);
-    const double val = __dadd_rn(d, CMP == 0 ? g0 : g1);
+    // diffusion row accumulated onto the reaction term: four FMAs and one add
+    const double val = fma(L.fa, x0, fma(L.fc, xm, fma(L.fb, xp, fma(L.fe, left + right, CMP == 0 ? g0 : g1))));
     if (h)
       out.y = val;
     else
@@ -243,14 +243,13 @@ __global__ void __launch_bounds__(NT, (3 - NBUF) * (256 / NT)) disk_ftheta_kerne
       for (int h = 0; h < 2; ++h) {
         const double x0 = h ? c2.y : c2.x, xm = h ? m2.y : m2.x, xp = h ? p2.y : p2.x;
         const double left = h ? c2.x : xl, right = h ? xr : c2.y;
-        const double d = fa * x0 + fc * xm + fb * xp + fe * (left + right);
         double u = CMP == 0 ? x0 : (h ? o2.y : o2.x);
         double v = CMP == 0 ? (h ? o2.y : o2.x) : x0;
         u = __dadd_rn(u, lift0);
         v = __dadd_rn(v, lift1);
         double g0, g1;
         reaction<KIN>(kin, u, v, g0, g1);
-        const double val = __dadd_rn(d, CMP == 0 ? g0 : g1);
+        const double val = fma(fa, x0, fma(fc, xm, fma(fb, xp, fma(fe, left + right, CMP == 0 ? g0 : g1))));
         if (h)
           out.y = val;
         else

@@ -743,12 +743,24 @@ int add_theta_stage(cg_plan* p, int epi, int src, int dst, int N, int A, int Bc,
   int rc = upload(p, h.data(), h.size(), &phif);
   if (rc) return rc;
   // scaled copy for the register FFT kernels: exact power-of-two factors
-  // (1/(2M) at j = 0, M; 1/(4M) otherwise), rows padded to an odd multiple of 8
+  // (1/(2M) at j = 0, M; 1/(4M) otherwise), rows padded to an odd multiple of
+  // 8; the pair (j, M - j) is stored as sum at j and difference at M - j, the
+  // self-paired M/2 doubled (thetafft.cuh split_pair)
   const int ps = phis_stride(M);
   std::vector<double> hs((size_t)p->NO * nclass * ps, 0.0);
-  for (size_t r = 0; r < (size_t)p->NO * nclass; ++r)
-    for (int j = 0; j <= M; ++j)
-      hs[r * ps + j] = h[r * (M + 1) + j] * ((j == 0 || j == M) ? 0.5 : 0.25) / (double)M;
+  for (size_t r = 0; r < (size_t)p->NO * nclass; ++r) {
+    auto scaled = [&](int j) { return h[r * (M + 1) + j] * ((j == 0 || j == M) ? 0.5 : 0.25) / (double)M; };
+    hs[r * ps] = scaled(0);
+    hs[r * ps + M] = scaled(M);
+    for (int j = 1; 2 * j <= M; ++j) {
+      if (2 * j == M) {
+        hs[r * ps + j] = 2.0 * scaled(j);
+      } else {
+        hs[r * ps + j] = scaled(j) + scaled(M - j);
+        hs[r * ps + M - j] = scaled(j) - scaled(M - j);
+      }
+    }
+  }
   double* phis = nullptr;
   if ((rc = upload(p, hs.data(), hs.size(), &phis))) return rc;
   st.phis = phis;
