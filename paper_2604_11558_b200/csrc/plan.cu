@@ -299,8 +299,11 @@ template <int GEOM, int KIN, int R2>
 int launch_fbuild_r(const StencilParams& p, cudaStream_t s, bool configure_only) {
   using S = FbuildShape<GEOM, R2>;
   if (configure_only) {  // at plan creation, never under stream capture
-    CUDA_TRY(cudaFuncSetAttribute(fbuild_rows_kernel<GEOM, KIN, R2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(fbuild_rows_kernel<GEOM, KIN, R2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024));
+    if constexpr (GEOM == 2)
+      CUDA_TRY(cudaFuncSetAttribute(fbuild_rows_kernel<GEOM, KIN, R2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    200 * 1024));
     return CG_OK;
   }
   if (p.batch > 65535) return fail(CG_EUNSUPPORTED, "batch > 65535 runs per plan");
@@ -311,7 +314,11 @@ int launch_fbuild_r(const StencilParams& p, cudaStream_t s, bool configure_only)
   const dim3 grid((unsigned)((p.n1 + S::RB - 1) / S::RB), S::D3 ? (unsigned)((p.n2 + S::JB - 1) / S::JB) : 1u,
                   (unsigned)p.batch);
   const unsigned threads = (unsigned)((nl + 31) / 32 * 32);
-  int rc = launch_pdl(fbuild_rows_kernel<GEOM, KIN, R2>, grid, dim3(threads), smem, s, p);
+  int rc;
+  if (GEOM == 2 && threads <= 128)  // the cylinder measured 9.7 us wide, 9.8 us narrow
+    rc = launch_pdl(fbuild_rows_kernel<GEOM, KIN, R2, GEOM == 2>, grid, dim3(threads), smem, s, p);
+  else
+    rc = launch_pdl(fbuild_rows_kernel<GEOM, KIN, R2, false>, grid, dim3(threads), smem, s, p);
   if (rc) return rc;
   CUDA_TRY(cudaGetLastError());
   return CG_OK;
@@ -873,6 +880,13 @@ int launch_theta(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
     if (tp.Bc == 1) {
       if (ax) return launch_pdl(theta_fast_kernel<5, 10, true, 100, true>, dim3(nb), dim3(100), F5::smem, s, tp);
       return launch_pdl(theta_fast_kernel<5, 10, false, 100, true>, dim3(nb), dim3(100), F5::smem, s, tp);
+    }
+    static const bool wide = getenv("CURVIGPU_T100_WIDE") != nullptr;  // A/B: 50 lines per 250-thread CTA
+    if (wide && span % 50 == 0) {
+      using F5w = FastTheta<5, 10, 250>;
+      const unsigned nbw = (unsigned)(lines / F5w::LPB);
+      if (ax) return launch_pdl(theta_fast_kernel<5, 10, true, 250>, dim3(nbw), dim3(250), F5w::smem, s, tp);
+      return launch_pdl(theta_fast_kernel<5, 10, false, 250>, dim3(nbw), dim3(250), F5w::smem, s, tp);
     }
     if (ax) return launch_pdl(theta_fast_kernel<5, 10, true, 100>, dim3(nb), dim3(100), F5::smem, s, tp);
     return launch_pdl(theta_fast_kernel<5, 10, false, 100>, dim3(nb), dim3(100), F5::smem, s, tp);
@@ -1594,6 +1608,11 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
                               (int)FastTheta<5, 10, 100>::smem);
     e2 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, false, 100>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)FastTheta<5, 10, 100>::smem);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
+    e1 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, true, 250>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)FastTheta<5, 10, 250>::smem);
+    e2 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, false, 250>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)FastTheta<5, 10, 250>::smem);
     if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
     e1 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, true, 100, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)FastTheta<5, 10, 100>::smem);

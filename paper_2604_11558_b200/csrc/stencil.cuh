@@ -139,7 +139,10 @@ struct FbuildShape {
 #ifndef CG_JB3
 #define CG_JB3 2
 #endif
-  static constexpr int RB = D3 ? CG_RB3 : R2;        // interior rows per CTA
+  // interior rows per CTA.  Ball: 5 (n_rho = 100: 20 x 50 = 1000 CTAs of 2.4
+  // staged rows per output row; 4 rows: 1250 CTAs of 2.5), with the narrow
+  // kernel's five CTAs per SM 12.5 -> 11.6 us (6 rows: 12.7 us)
+  static constexpr int RB = D3 ? (GEOM == 2 ? 5 : CG_RB3) : R2;
   // 3-D: JB consecutive theta columns per CTA share their theta neighbours:
   // staged rows = JB (RB + 2) centre rows + 2 RB theta-halo rows.  JB = 2
   // (2.5 staged rows per output row instead of 3.5): cylinder F-build
@@ -155,6 +158,23 @@ struct FbuildShape {
 // (offsets within one field are 32-bit: a field holds < 2^31 elements, checked
 // at plan creation; 64-bit index arithmetic per load made the 3-D kernels
 // issue-bound)
+// One staged value.  ASYNC: an 8-byte cp.async (no register round trip; the
+// cylinder's F-build 10.2 -> 9.7 us, no gain for the ball or the 2-D kernels,
+// profiles/r02_fbuild_ab.txt), closed by stage_wait before the CTA barrier.
+template <bool ASYNC>
+__device__ __forceinline__ void stage_put(double* dst, const double* src) {
+  if constexpr (ASYNC)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  else
+    *dst = __ldg(src);
+}
+template <bool ASYNC>
+__device__ __forceinline__ void stage_wait() {
+  if constexpr (ASYNC) asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+template <int GEOM>
+constexpr bool kStageAsync = (GEOM == 3);
+
 template <int GEOM, int R2 = 8>
 __device__ __forceinline__ void stage_rows(double* s, const double* __restrict__ X, int i0, int j, int n1, int n2,
                                            int nl, int rs, int jst) {
@@ -171,7 +191,7 @@ __device__ __forceinline__ void stage_rows(double* s, const double* __restrict__
       int i = i0 - 1 + r;
       if (i < 0) i = periodic_walk ? n1 - 1 : 0;
       if (i >= n1) i = periodic_walk ? i - n1 : n1 - 1;
-      s[(jj * (S::RB + 2) + r) * nl + l] = __ldg(X + (i * rs + jo + l));
+      stage_put<kStageAsync<GEOM>>(&s[(jj * (S::RB + 2) + r) * nl + l], X + (i * rs + jo + l));
     }
   }
   if (S::D3) {
@@ -181,8 +201,8 @@ __device__ __forceinline__ void stage_rows(double* s, const double* __restrict__
 #pragma unroll
     for (int r = 0; r < S::RB; ++r) {
       const int i = min(i0 + r, n1 - 1);
-      s[(H + r) * nl + l] = __ldg(X + (i * rs + (jm - j) * jst + l));
-      s[(H + S::RB + r) * nl + l] = __ldg(X + (i * rs + (jp - j) * jst + l));
+      stage_put<kStageAsync<GEOM>>(&s[(H + r) * nl + l], X + (i * rs + (jm - j) * jst + l));
+      stage_put<kStageAsync<GEOM>>(&s[(H + S::RB + r) * nl + l], X + (i * rs + (jp - j) * jst + l));
     }
   }
 }
@@ -280,8 +300,10 @@ __device__ __forceinline__ void row_coefs(RowCoef* rcs, const StencilParams& p, 
   }
 }
 
-template <int GEOM, int KIN, int R2 = 8>
-__global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p) {
+// NARROW (3-D fields whose contiguous axis fits 128 threads): capped at 96
+// registers so five CTAs share an SM (ball 12.5 -> 11.8 us with 4-row CTAs)
+template <int GEOM, int KIN, int R2 = 8, bool NARROW = false>
+__global__ void __launch_bounds__(NARROW ? 128 : 512, NARROW ? 5 : 1) fbuild_rows_kernel(const StencilParams p) {
   using S = FbuildShape<GEOM, R2>;
   extern __shared__ double fb_smem[];
   __shared__ RowCoef rcs[8 * S::RB];  // up to 8 components
@@ -309,6 +331,7 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
       const double* X = p.W + wbase + (long long)c * p.npw;
       if (c > 0) __syncthreads();
       stage_rows<GEOM, R2>(fb_smem, X, i0, j, n1, p.n2, nl, rsw, p.ldw);
+      stage_wait<kStageAsync<GEOM>>();
       __syncthreads();
       if (l < nl) {
         const CompCoef k = comp_coef<GEOM>(p, ob + c, l, nl);
@@ -342,6 +365,7 @@ __global__ void __launch_bounds__(512) fbuild_rows_kernel(const StencilParams p)
     for (int q = 0; q < 9; ++q) kin[q] = (q < p.nparams) ? p.kin[(long long)b * p.nparams + q] : 0.0;
     const double lift0 = lift_addend(p.lift[0]), lift1 = lift_addend(p.lift[1]);
     const bool with_r = p.with_reaction;
+    stage_wait<kStageAsync<GEOM>>();
     __syncthreads();
     if (l >= nl) return;
     double* __restrict__ Fo = p.F + fbase;       // species 0 of this CTA's run / theta column
