@@ -854,19 +854,24 @@ int launch_theta(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const bool small_cta = !getenv("CURVIGPU_NO_SMALL_CTA");
+  // column kernels stage the N twiddles and their lines' Phi rows (one row when every line of a CTA
+  // shares its class) behind the FFT tile; FastTheta::smem_cols is the opt-in maximum
+  auto cols_smem = [&](size_t tile, int lpb, int ps) {
+    return tile + (size_t)st.N * sizeof(double2) + (size_t)(tp.phi_class_a == 1 ? 1 : lpb) * ps * sizeof(double);
+  };
 #define TRY_FAST_R(M1, M2, R)                                                                        \
   {                                                                                                  \
     using F64 = FastTheta<M1, M2, 64>;                                                               \
     if (small_cta && lines / FastTheta<M1, M2>::LPB < sms && span % F64::LPB == 0) {                  \
       const unsigned nb = (unsigned)(lines / F64::LPB);                                              \
       if (ax)                                                                                        \
-        return launch_pdl(theta_fast_kernel<M1, M2, true, 64, R>, dim3(nb), dim3(64), F64::smem, s, tp);  \
-      return launch_pdl(theta_fast_kernel<M1, M2, false, 64, R>, dim3(nb), dim3(64), F64::smem, s, tp);   \
+        return launch_pdl(theta_fast_kernel<M1, M2, true, 64, R>, dim3(nb), dim3(64), (R) ? F64::smem : cols_smem(F64::smem, F64::LPB, F64::PS), s, tp);  \
+      return launch_pdl(theta_fast_kernel<M1, M2, false, 64, R>, dim3(nb), dim3(64), (R) ? F64::smem : cols_smem(F64::smem, F64::LPB, F64::PS), s, tp);   \
     }                                                                                                \
     const unsigned nb = (unsigned)(lines / FastTheta<M1, M2>::LPB);                                  \
     if (ax)                                                                                          \
-      return launch_pdl(theta_fast_kernel<M1, M2, true, 256, R>, dim3(nb), dim3(256), FastTheta<M1, M2>::smem, s, tp); \
-    return launch_pdl(theta_fast_kernel<M1, M2, false, 256, R>, dim3(nb), dim3(256), FastTheta<M1, M2>::smem, s, tp); \
+      return launch_pdl(theta_fast_kernel<M1, M2, true, 256, R>, dim3(nb), dim3(256), (R) ? FastTheta<M1, M2>::smem : cols_smem(FastTheta<M1, M2>::smem, FastTheta<M1, M2>::LPB, FastTheta<M1, M2>::PS), s, tp); \
+    return launch_pdl(theta_fast_kernel<M1, M2, false, 256, R>, dim3(nb), dim3(256), (R) ? FastTheta<M1, M2>::smem : cols_smem(FastTheta<M1, M2>::smem, FastTheta<M1, M2>::LPB, FastTheta<M1, M2>::PS), s, tp); \
   }
 #define TRY_FAST(M1, M2)                                                                             \
   if (st.N / 2 == (M1) * (M2) && span % FastTheta<M1, M2>::LPB == 0) {                               \
@@ -880,13 +885,6 @@ int launch_theta(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
     if (tp.Bc == 1) {
       if (ax) return launch_pdl(theta_fast_kernel<5, 10, true, 100, true>, dim3(nb), dim3(100), F5::smem, s, tp);
       return launch_pdl(theta_fast_kernel<5, 10, false, 100, true>, dim3(nb), dim3(100), F5::smem, s, tp);
-    }
-    static const bool wide = getenv("CURVIGPU_T100_WIDE") != nullptr;  // A/B: 50 lines per 250-thread CTA
-    if (wide && span % 50 == 0) {
-      using F5w = FastTheta<5, 10, 250>;
-      const unsigned nbw = (unsigned)(lines / F5w::LPB);
-      if (ax) return launch_pdl(theta_fast_kernel<5, 10, true, 250>, dim3(nbw), dim3(250), F5w::smem, s, tp);
-      return launch_pdl(theta_fast_kernel<5, 10, false, 250>, dim3(nbw), dim3(250), F5w::smem, s, tp);
     }
     if (ax) return launch_pdl(theta_fast_kernel<5, 10, true, 100>, dim3(nb), dim3(100), F5::smem, s, tp);
     return launch_pdl(theta_fast_kernel<5, 10, false, 100>, dim3(nb), dim3(100), F5::smem, s, tp);
@@ -1594,25 +1592,20 @@ int cg_plan_create(const cg_desc* d, cg_plan** out) {
     if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
 #define OPT_IN_R(M1, M2, R)                                                                                   \
   e1 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, true, 256, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,\
-                            (int)FastTheta<M1, M2>::smem);                                                    \
+                            (int)FastTheta<M1, M2>::smem_cols);                                               \
   e2 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, false, 256, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,\
-                            (int)FastTheta<M1, M2>::smem);                                                    \
+                            (int)FastTheta<M1, M2>::smem_cols);                                               \
   if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));  \
   e1 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, true, 64, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                            (int)FastTheta<M1, M2, 64>::smem);                                                \
+                            (int)FastTheta<M1, M2, 64>::smem_cols);                                           \
   e2 = cudaFuncSetAttribute(theta_fast_kernel<M1, M2, false, 64, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,\
-                            (int)FastTheta<M1, M2, 64>::smem);                                                \
+                            (int)FastTheta<M1, M2, 64>::smem_cols);                                           \
   if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
 #define OPT_IN(M1, M2) OPT_IN_R(M1, M2, false) OPT_IN_R(M1, M2, true)
     e1 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, true, 100>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)FastTheta<5, 10, 100>::smem);
     e2 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, false, 100>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)FastTheta<5, 10, 100>::smem);
-    if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
-    e1 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, true, 250>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)FastTheta<5, 10, 250>::smem);
-    e2 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, false, 250>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)FastTheta<5, 10, 250>::smem);
     if (e1 != cudaSuccess || e2 != cudaSuccess) return bail(fail(CG_ECUDA, "theta kernel smem opt-in failed"));
     e1 = cudaFuncSetAttribute(theta_fast_kernel<5, 10, true, 100, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)FastTheta<5, 10, 100>::smem);

@@ -420,6 +420,10 @@ struct FastTheta {
   static constexpr int SL0 = LDT > M ? LDT : M;
   static constexpr int SL = (SL0 % 2 == 0) ? SL0 + 1 : SL0;  // odd line stride: lines land on distinct banks
   static constexpr size_t smem = (size_t)LPB * SL * sizeof(double2);
+  // column kernels (theta_fast_kernel, !ROWS) also stage the N twiddles and
+  // their lines' scaled Phi rows (row stride PS = plan.cu phis_stride(M))
+  static constexpr int PS = ((M + 1 + 7) / 8 * 8) % 16 == 0 ? (M + 1 + 7) / 8 * 8 + 8 : (M + 1 + 7) / 8 * 8;
+  static constexpr size_t smem_cols = smem + (size_t)2 * M * sizeof(double2) + (size_t)LPB * PS * sizeof(double);
 };
 
 // table read: read-only global path, or shared memory (TS) when a kernel
@@ -494,7 +498,9 @@ __device__ __forceinline__ double2 shfl_d2(double2 v, int src) {
 // column slabs of the CTAs that own the columns -- base = line * N with lines
 // ordered [species][4 rows of cluster rank r], column pair 2k goes to CTA k / 4
 // at [species][rho row][2k % 8].
-template <int M1, int M2, bool AXPY, bool TS = false, bool RS = false, int BCM = 0, bool CLS = false>
+// TWA: with TS, twa holds the phase-A twiddles as a [M1][M2] table (the disk
+// front); without it phase A reads them from the staged length-N table tw.
+template <int M1, int M2, bool AXPY, bool TS = false, bool RS = false, int BCM = 0, bool CLS = false, bool TWA = TS>
 __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int lt, const double* ph,
                                            const double2* tw, int f, long long base, long long es, int Bc,
                                            const double2* twa = nullptr) {
@@ -579,10 +585,10 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
       double2 col[M1];
 #pragma unroll
       for (int n1 = 0; n1 < M1; ++n1) col[n1] = keep[q + (M2 / M1) * n1];
-      if (TS)
+      if constexpr (TWA)
         phase_a<M1, M2, true, true, true>(col, S, lt + q * TPL, twa);
       else
-        phase_a<M1, M2, true>(col, S, lt + q * TPL, tw);
+        phase_a<M1, M2, true, TS>(col, S, lt + q * TPL, tw);
     }
   } else {
   // ---------------- forward phase B: rows k1 = lt, lt + TPL, ...
@@ -642,10 +648,10 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < M2 / TPL; ++q) {
-    if (TS)
+    if constexpr (TWA)
       phase_a<M1, M2, true, true, true>(keepa[q], S, lt + q * TPL, twa);
     else
-      phase_a<M1, M2, true>(keepa[q], S, lt + q * TPL, tw);
+      phase_a<M1, M2, true, TS>(keepa[q], S, lt + q * TPL, tw);
   }
   }  // RS
   if constexpr (RS && !kTailCtaSync)
@@ -727,9 +733,22 @@ __device__ __forceinline__ void theta_tail(const ThetaParams& p, double2* S, int
 
 // ROWS: lines are contiguous rows (Bc == 1), a compile-time split so the
 // column kernels (Bc > 1) keep their own register allocation
-template <int M1, int M2, bool AXPY, int NT = 256, bool ROWS = false>
+// STG (column kernels): the N twiddles and the CTA's scaled Phi rows are plan
+// constants, copied to shared memory by cp.async before the wait on the
+// previous kernel, so the split / merge and both phase A passes read them at
+// shared-memory latency instead of L2 latency in the middle of the dependent
+// chain (ncu: long_scoreboard was 7.5 of 12 stall cycles per issue in the
+// ball's kernel).  A CTA's lines have consecutive Phi classes (one class for
+// phi_class_a == 1), so its rows are one contiguous block.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Measured (profiles/r02_theta_staging.txt): sphere 6.28 -> 5.14 us, cylinder
+// 10.85 -> 9.98 us; the ball's 100-point kernel (a Phi row per line, 9 KB per
+// CTA) 12.2 -> 13.2 us, so the 5 x 10 kernels keep reading through L1.
+template <int M1, int M2, bool AXPY, int NT = 256, bool ROWS = false, bool STG = !ROWS && (M1 != 5)>
 __global__ void __launch_bounds__(NT) theta_fast_kernel(const ThetaParams p) {
-  pdl_wait();
   using F = FastTheta<M1, M2, NT>;
   constexpr int M = F::M, TPL = F::TPL, LPB = F::LPB;
   extern __shared__ double2 tf_smem[];
@@ -765,6 +784,25 @@ __global__ void __launch_bounds__(NT) theta_fast_kernel(const ThetaParams p) {
   }
   const int c = f % p.ncomp;
   const int la = rows ? a0 + ln : a0, lbc = rows ? 0 : bc0 + ln;
+  const int cls = p.phi_class_a == 1 ? la : (p.phi_class_a == 0 ? lbc : la * Bc + lbc);
+  const double* ph = p.phis + ((long long)c * p.nclass + cls) * p.phis_ld;
+  const double2* tw = p.tw;
+  if constexpr (STG) {
+    double2* tw_s = tf_smem + LPB * F::SL;
+    double* ph_s = reinterpret_cast<double*>(tw_s + N);
+    const bool one = rows || p.phi_class_a == 1;  // every line of the CTA in one class (rows: never staged)
+    const int cls0 = p.phi_class_a == 1 ? a0 : (p.phi_class_a == 0 ? bc0 : a0 * Bc + bc0);
+    const double* src = p.phis + ((long long)c * p.nclass + cls0) * F::PS;  // PS == p.phis_ld (checked at plan set-up)
+    const int chunks = (one ? 1 : LPB) * (F::PS / 2);
+    for (int i = tid; i < N; i += NT) cp_async16(tw_s + i, p.tw + i);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");  // group 1: twiddles (needed by phase A)
+    for (int i = tid; i < chunks; i += NT) cp_async16(ph_s + 2 * i, src + 2 * i);
+    ph = ph_s + (one ? 0 : ln * F::PS);  // (unconditionally a shared-space pointer: a run-time choice
+                                         // between the staged and the global row made every Phi load generic)
+    asm volatile("cp.async.commit_group;\n" ::: "memory");  // group 2: Phi rows (needed by the split)
+    tw = tw_s;
+  }
+  pdl_wait();
   const long long lstride = (long long)N * Bc;
   const long long base = (long long)f * p.npts + (long long)la * lstride + lbc;  // element t at base + t*es
   const long long es = Bc;
@@ -784,13 +822,17 @@ __global__ void __launch_bounds__(NT) theta_fast_kernel(const ThetaParams p) {
         keepa[q][n1] = make_double2(__ldg(p.X + base + (2LL * k) * es), __ldg(p.X + base + (2LL * k + 1) * es));
     }
   }
+  if constexpr (STG) {
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncthreads();  // the staged twiddles are visible to every thread
+  }
 #pragma unroll
-  for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, false>(keepa[q], S, lt + q * TPL, p.tw);
-  const int cls = p.phi_class_a == 1 ? la : (p.phi_class_a == 0 ? lbc : la * Bc + lbc);
-  const double* ph = p.phis + ((long long)c * p.nclass + cls) * p.phis_ld;
+  for (int q = 0; q < M2 / TPL; ++q) phase_a<M1, M2, false, STG>(keepa[q], S, lt + q * TPL, tw);
+  // the Phi rows had phase A to land; theta_tail's first barrier publishes them
+  if constexpr (STG) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   // contiguous lines (Bc == 1) keep a line's threads in consecutive lanes: register split
   constexpr bool RS = ROWS && (TPL == M1) && ((TPL & (TPL - 1)) == 0) && TPL <= 32;
-  theta_tail<M1, M2, AXPY, false, RS, MODE>(p, S, lt, ph, p.tw, f, base, es, Bc);
+  theta_tail<M1, M2, AXPY, STG, RS, MODE, false, false>(p, S, lt, ph, tw, f, base, es, Bc);
 }
 
 }  // namespace cg
