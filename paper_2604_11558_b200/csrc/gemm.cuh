@@ -58,6 +58,7 @@ struct GemmParams {
   double tau, limit;
   int* first_bad;   // [nfield] smallest diverged step (atomicMin)
   const int* step;  // current step number (device)
+  int tma_partial;  // partial tiles leave by the (clipping) bulk tensor store too
 };
 
 template <int BM, int BN>
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
       auto store_prev = [&](int ptc) {
         mbar_wait(epi_ready, ptc & 1);
         // partial tiles (and every CHAIN tile: etile holds its intermediate) were stored from registers
-        if (EPI != EPI_CHAIN && (pm0 + BM <= p.M) && (pn0 + BN <= p.N)) {
+        if (EPI != EPI_CHAIN && (p.tma_partial || ((pm0 + BM <= p.M) && (pn0 + BN <= p.N)))) {
           tma_store_4d(&mapO, etile, pn0, pm0, ps, pf);
           bulk_commit();
         }
@@ -420,12 +421,18 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
         using KS_ON = std::true_type;
         using KS_OFF = std::false_type;
         if constexpr (SKIP) {
-          static_assert(MT == 2, "ragged tiles: two 8-row blocks per warp");
           const int ml = (p.M - m0 - wm0 + 7) >> 3;  // live 8-row blocks of this warp
-          if (ml >= 2)
-            slice(std::integral_constant<int, 2>{}, KS_ON{});
-          else if (ml == 1)
-            slice(std::integral_constant<int, 1>{}, KS_ON{});
+          // warp-uniform dispatch to the instantiation with min(ml, MT) live blocks
+          auto pick = [&](auto self, auto live) -> void {
+            constexpr int V = decltype(live)::value;
+            if constexpr (V >= 1) {
+              if (ml >= V)
+                slice(std::integral_constant<int, V>{}, KS_ON{});
+              else
+                self(self, std::integral_constant<int, V - 1>{});
+            }
+          };
+          pick(pick, std::integral_constant<int, MT>{});
         } else {
           slice(std::integral_constant<int, MT>{}, KS_OFF{});
         }
@@ -519,9 +526,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + 32, MINB)
     // clipped bulk tensor store of such tiles measured nondeterministic on
     // B200 with two CTAs per SM (tools/chain_dbg2.py); full tiles use TMA.
     // CHAIN: etile holds the intermediate other warps may still be reading
-    const bool full_tile = EPI != EPI_CHAIN && (m0 + BM <= p.M) && (n0 + BN <= p.N);
+    const bool full_tile = EPI != EPI_CHAIN && (p.tma_partial || ((m0 + BM <= p.M) && (n0 + BN <= p.N)));
     // Phi1 operands for EPI_PHI (L2-resident table), all loads in flight per row group
-    constexpr int EC = (MINB >= 2 && MT > 2) ? MT / 2 : MT;
+    constexpr int EC = (MINB >= 2 && MT > 2 && MT % 2 == 0) ? MT / 2 : MT;
 #pragma unroll
     for (int i0 = 0; i0 < MT; i0 += EC) {
       double2 ph[EC][NT];

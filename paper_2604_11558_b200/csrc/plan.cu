@@ -127,17 +127,22 @@ int make_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
 struct TileCfg {
   int BM, BN;
 };
-constexpr int kNumCfg = 18;
+constexpr int kNumCfg = 20;
 constexpr int kChainCfg = 14;  // EPI_CHAIN only: 32 rows x all (<= 128) columns, 8 warps of 16x32
 constexpr int kChainCfg16 = 15;  // EPI_CHAIN, 16-row tiles on 4 warps at 3 CTAs/SM (CURVIGPU_CHAIN_CFG=15)
 constexpr int kRaggedCfg = 16;   // cfg 12 for NN stages with M or K off the tile grid (zero-block skips)
 constexpr int kWideCfg = 17;     // 16 x 128 tiles (4 warps of 16x32, 3 CTAs/SM) for TN stages with N = 128
+// NN stages whose operator has at most 112 rows (n = 100): one m tile of 112 x 32 on two consumer warps of
+// 112 x 16 (up to 14 live 8-row blocks each: 16 fragment loads per 28 DMMAs instead of 4 per 4, no quarter-empty
+// last m tile).  18: 4-stage ring, 2 CTAs/SM; 19: 2-stage ring, 3 CTAs/SM.
+constexpr int kTallCfg = 18;
+constexpr int kTallCfg3 = 19;
 // 7, 8: the 64x64 configuration split-K over clusters of 2 / 4 CTAs
 // 9, 10: 64x64 tiles on 8 consumer warps (32x16 / 16x32 warp tiles); 11: 10 split-K over 2-CTA clusters
 // 12: 32x32 tiles on 4 warps of 16x16 (stages with very few 64x64 tiles); 13: 12 split-K over 2-CTA clusters
 constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {64, 128}, {128, 128}, {64, 64},
                                     {64, 64}, {64, 64}, {64, 64}, {64, 64}, {64, 64},
-                                    {32, 32}, {32, 32}, {32, 128}, {16, 128}, {32, 32}, {16, 128}};
+                                    {32, 32}, {32, 32}, {32, 128}, {16, 128}, {32, 32}, {16, 128}, {112, 32}, {112, 32}};
 
 // BM, BN, warp tile, stages; 32x32 warp tiles keep the accumulators +
 // fragments under ~160 registers without spills.
@@ -154,6 +159,8 @@ constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {
 #define CFG12 32, 32, 16, 16, 4, 4
 #define CFG14 32, 128, 16, 32, 3, 2
 #define CFG15 16, 128, 16, 32, 3, 3
+#define CFG18 112, 32, 56, 16, 4, 2
+#define CFG19 112, 32, 56, 16, 2, 3
 
 // configure_only: set the dynamic shared memory opt-in (done at plan
 // creation, never inside a stream capture).  KS > 1 launches clusters of KS
@@ -254,6 +261,12 @@ int launch_gemm_cfg(int cfg, const Maps& m, const GemmParams& p, cudaStream_t st
     case 13: return launch_gemm_t<VAR, CFG12, EPI, 2>(m.a, m.b, m.w, m.o, p, stream, conf);
     case 16: return launch_gemm_t<VAR, CFG12, EPI, 1, VAR == VAR_NN>(m.a, m.b, m.w, m.o, p, stream, conf);
     case 17: return launch_gemm_t<VAR, CFG15, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
+    case kTallCfg:
+      if constexpr (VAR == VAR_NN) return launch_gemm_t<VAR, CFG18, EPI, 1, true>(m.a, m.b, m.w, m.o, p, stream, conf);
+      return fail(CG_EINVAL, "tall tiles are an NN configuration");
+    case kTallCfg3:
+      if constexpr (VAR == VAR_NN) return launch_gemm_t<VAR, CFG19, EPI, 1, true>(m.a, m.b, m.w, m.o, p, stream, conf);
+      return fail(CG_EINVAL, "tall tiles are an NN configuration");
     default: return launch_gemm_t<VAR, CFG6, EPI>(m.a, m.b, m.w, m.o, p, stream, conf);
   }
 }
@@ -625,6 +638,7 @@ int pick_cfg(int var, long long nbatch, int M, int N, int K, int stage_index) {
     }
     const int v = nv == 1 ? vals[0] : (stage_index < nv ? vals[stage_index] : -1);
     if ((v >= 0 && v < kChainCfg) || v == 17) return v;
+    if ((v == kTallCfg || v == kTallCfg3) && var == VAR_NN && M <= 112) return v;
   }
   // Measured on B200 with the TMA epilogue (tools/sweep_tiles.py,
   // profiles/r01_tile_sweep_tmaepi.txt): 64x64 tiles, 4-stage ring, 2 CTAs/SM
@@ -978,6 +992,8 @@ int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
     gp.limit = 1e12;  // DIVERGENCE_LIMIT, integrators.py:33
     gp.first_bad = first_bad;
     gp.step = p->step_dev;
+    static const bool tma_partial = getenv("CURVIGPU_TMA_PARTIAL") != nullptr;  // A/B
+    gp.tma_partial = tma_partial ? 1 : 0;
     Maps mp;
     mp.a = (st.var == VAR_TN) ? smap : st.opmap;
     mp.b = (st.var == VAR_TN) ? st.opmap : smap;

@@ -45,14 +45,18 @@ def stage_output(plan, st, W, out):
 
 def main():
     os.environ["CURVIGPU_LANES"] = "1"
-    for cfg in (None, "resident", "2", "7", "8", "9", "11", "12", "13", "15"):
+    cfgs = (None, "resident", "2", "7", "8", "9", "11", "12", "13", "15", "18", "19")
+    if os.environ.get("RS_CFGS"):  # e.g. RS_CFGS=default,12,18 RS_CONFIGS=4
+        cfgs = tuple(None if c == "default" else c for c in os.environ["RS_CFGS"].split(","))
+    ks = tuple(int(c) for c in os.environ.get("RS_CONFIGS", "1,2,3,4,5").split(","))
+    for cfg in cfgs:
         os.environ.pop("CURVIGPU_TILE_CFG", None)
         os.environ.pop("CURVIGPU_RESIDENT", None)
         if cfg == "resident":  # every eligible stage through the resident-operator kernel
             os.environ["CURVIGPU_RESIDENT"] = "1"
         elif cfg:
             os.environ["CURVIGPU_TILE_CFG"] = cfg
-        for k in (1, 2, 3, 4, 5):
+        for k in ks:
             for theta in ("fft", "gemm"):
                 if cfg and cfg != "resident" and k == 5:
                     continue
@@ -104,4 +108,5 @@ def cluster_runs():
 
 if __name__ == "__main__":
     main()
-    cluster_runs()
+    if not os.environ.get("RS_CFGS"):
+        cluster_runs()
