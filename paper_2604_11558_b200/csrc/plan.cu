@@ -992,7 +992,7 @@ int launch_stage(cg_plan* p, const Stage& st, const double* Win, double* Wout, i
     gp.limit = 1e12;  // DIVERGENCE_LIMIT, integrators.py:33
     gp.first_bad = first_bad;
     gp.step = p->step_dev;
-    static const bool tma_partial = getenv("CURVIGPU_TMA_PARTIAL") != nullptr;  // A/B
+    const bool tma_partial = getenv("CURVIGPU_TMA_PARTIAL") != nullptr;  // measurement / test switch (profiles/r02_tma_partial.txt)
     gp.tma_partial = tma_partial ? 1 : 0;
     Maps mp;
     mp.a = (st.var == VAR_TN) ? smap : st.opmap;

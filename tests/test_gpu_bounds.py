@@ -56,7 +56,7 @@ CASES = [
     (3, (4, 6, 9), {}), (4, (10, 12, 10), {}), (4, (5, 6, 7), {}), (4, (6, 8, 128), {}),
     (4, (100, 100, 100), {}), (4, (10, 12, 10), {"CURVIGPU_NO_CHAIN": "1"}),
     (4, (10, 12, 10), {"CURVIGPU_CHAIN_CFG": "15"}),
-] + [(k, d, {"CURVIGPU_TILE_CFG": c}) for c in ("2", "7", "8", "9", "11", "12", "13")
+] + [(k, d, {"CURVIGPU_TILE_CFG": c}) for c in ("2", "7", "8", "9", "11", "12", "13", "18", "19")
      for k, d in ((2, (24, 16)), (4, (10, 12, 10)))]
 
 

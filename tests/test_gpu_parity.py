@@ -372,7 +372,7 @@ def test_odd_contiguous_axis_runs_match_oracle(k, dims):
         assert rel_inf(res.fields[c.name], ref[c.name]) <= STEP1_TOL, c.name
 
 
-@pytest.mark.parametrize("cfg", ["2", "7", "8", "9", "11", "12", "13"])
+@pytest.mark.parametrize("cfg", ["2", "7", "8", "9", "11", "12", "13", "18", "19"])
 @pytest.mark.parametrize("k,dims", [(2, (24, 16)), (4, (10, 12, 10)), (1, (16, 32)), (3, (8, 16, 16))])
 def test_cluster_split_k_gemm_matches_oracle_and_reruns(monkeypatch, cfg, k, dims):
     """Every GEMM stage forced onto one tile configuration: the split-K cluster
@@ -380,7 +380,9 @@ def test_cluster_split_k_gemm_matches_oracle_and_reruns(monkeypatch, cfg, k, dim
     8-warp CTAs, partials reduced over DSMEM in rank order), incl.
     ranks with no k slice at all (K = 16 with 2 or 4 ranks), and the
     non-default single-CTA tiles (cfg 2: 4 warps of 32x32, cfg 9: 8 warps of
-    32x16): same results as the oracle within the single-op tolerance and
+    32x16; cfg 18 / 19: the 112-row "tall" tiles of the NN stages, whose warps
+    skip their dead 8-row blocks -- TN stages keep their default under these
+    two): same results as the oracle within the single-op tolerance and
     bitwise-identical reruns."""
     monkeypatch.setenv("CURVIGPU_TILE_CFG", cfg)
     sysm = pcfg.BUILDERS[k](dims)
@@ -523,3 +525,21 @@ def test_ball_with_100_theta_points_and_any_polar_extent_matches_the_oracle(dims
     ref = orc.physical(osys, orc.integrate(osys, 4, 0.04))
     for name in ref:
         assert rel_inf(got[name], ref[name]) <= 1e-12, (dims, name)
+
+
+@pytest.mark.parametrize("cfg", [None, "19"])
+def test_clipped_tma_store_of_partial_tiles_matches_register_path(monkeypatch, theta_mode, cfg):
+    """CURVIGPU_TMA_PARTIAL=1 sends partial GEMM tiles through the clipping bulk
+    tensor store instead of bounds-checked register stores (re-tested with the
+    stage-ring proxy fence in place, profiles/r02_tma_partial.txt): the same
+    values bit for bit on a ball with ragged extents, default and tall tiles."""
+    if cfg:
+        monkeypatch.setenv("CURVIGPU_TILE_CFG", cfg)
+    sysm = pcfg.BUILDERS[4]((36, 20, 28))
+    a = run_simulation(sysm, 12, 0.12)
+    monkeypatch.setenv("CURVIGPU_TMA_PARTIAL", "1")
+    b = run_simulation(sysm, 12, 0.12)
+    c2 = run_simulation(sysm, 12, 0.12)
+    for c in sysm.components:
+        assert np.array_equal(a.fields[c.name], b.fields[c.name]), c.name
+        assert np.array_equal(b.fields[c.name], c2.fields[c.name]), c.name
