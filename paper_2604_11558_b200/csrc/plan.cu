@@ -156,7 +156,16 @@ constexpr TileCfg kCfgs[kNumCfg] = {{128, 64}, {64, 128}, {64, 64}, {128, 64}, {
 #define CFG6 64, 64, 32, 32, 6, 3
 #define CFG9 64, 64, 32, 16, 4, 2
 #define CFG10 64, 64, 16, 32, 4, 2
-#define CFG12 32, 32, 16, 16, 4, 4
+// 32x32 tiles: 4-stage ring at FIVE CTAs per SM (41 KB, 70 registers): 20 consumer warps per SM instead of 16 --
+// ball rho 21.2 -> 19.9 us, its DMMA-theta stages 30.6 / 27.2 -> 28.7 / 25.4 us, cylinder rho 13.1 -> 12.9 us;
+// six CTAs (3 stages, 64 registers) measured 21.4 us (profiles/r02_cfg12_occupancy.txt)
+#ifndef CG_CFG12_ST
+#define CG_CFG12_ST 4
+#endif
+#ifndef CG_CFG12_MINB
+#define CG_CFG12_MINB 5
+#endif
+#define CFG12 32, 32, 16, 16, CG_CFG12_ST, CG_CFG12_MINB
 #define CFG14 32, 128, 16, 32, 3, 2
 #define CFG15 16, 128, 16, 32, 3, 3
 #define CFG18 112, 32, 56, 16, 4, 2
